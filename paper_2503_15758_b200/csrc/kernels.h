@@ -1,0 +1,30 @@
+// kernels.h — internal launcher declarations shared by the .cu files.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "../../include/attn2d_b200.h"
+
+namespace a2d {
+
+// error plumbing (abi.cu)
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(cudaError_t e, const char* what);
+int check_launch(const char* what);
+
+int launch_tile_fwd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                    const CUtensorMap& tv, cudaStream_t stream);
+int launch_tile_bwd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                    const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream);
+int launch_lse_merge(const float* o_parts, const float* lse_parts, int k_parts,
+                     long long part_stride_o, long long part_stride_lse, long long rows, int h,
+                     long long row_stride, void* o_out, int out_dtype, long long out_row_stride,
+                     float* lse_out, cudaStream_t stream);
+int launch_bwd_preprocess(const void* o, const void* dout, float* delta, long long o_sbh,
+                          long long o_srow, long long do_sbh, long long do_srow, int bh, int n,
+                          int h, cudaStream_t stream);
+int launch_bwd_finalize(const float* dq_acc, void* dq, int out_dtype, long long sbh,
+                        long long srow, int bh, int n, int h, float scale, cudaStream_t stream);
+int launch_selftest_umma(const void* a, const void* b, float* d, int n, int b_mn_major,
+                         cudaStream_t stream);
+
+}  // namespace a2d

@@ -1,0 +1,99 @@
+// selftest.cu — one-CTA tcgen05 GEMM used to pin the UMMA descriptor
+// encodings (K-major and MN-major SWIZZLE_128B operands) on the device.
+#include "sm100.cuh"
+#include "kernels.h"
+
+namespace a2d {
+namespace {
+
+constexpr int SLAB = 128 * 128;  // 128 rows x 128 B
+
+// element (m, k) of a K-major SW128 operand with 128 rows per slab
+__device__ __forceinline__ uint32_t kmajor_off(int m, int k) {
+  return (k >> 6) * SLAB + m * 128 + ((((k & 63) >> 3) ^ (m & 7)) << 4) + (k & 7) * 2;
+}
+// element (k, n) of an MN-major SW128 operand with 128 k-rows per 64-wide atom
+__device__ __forceinline__ uint32_t mnmajor_off(int k, int n) {
+  return (n >> 6) * SLAB + k * 128 + ((((n & 63) >> 3) ^ (k & 7)) << 4) + (n & 7) * 2;
+}
+
+__global__ void __launch_bounds__(128, 1)
+    selftest_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b, float* d, int n, int b_mn) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sa = smem_u32(smem);
+  const uint32_t sbb = sa + 2 * SLAB;
+  const uint32_t sbar = sbb + 2 * SLAB;
+  const uint32_t stm = sbar + 8;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 128 * 128; i += blockDim.x) {
+    const int m = i / 128, k = i % 128;
+    *reinterpret_cast<__nv_bfloat16*>(smem + kmajor_off(m, k)) = a[i];
+  }
+  for (int i = threadIdx.x; i < 128 * n; i += blockDim.x) {
+    if (b_mn) {  // b given as [k][n]
+      const int k = i / n, nn = i % n;
+      *reinterpret_cast<__nv_bfloat16*>(smem + 2 * SLAB + mnmajor_off(k, nn)) = b[i];
+    } else {     // b given as [n][k]
+      const int nn = i / 128, k = i % 128;
+      *reinterpret_cast<__nv_bfloat16*>(smem + 2 * SLAB + kmajor_off(nn, k)) = b[i];
+    }
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(sbar, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  if (warp == 0) {
+    tmem_alloc(stm, 128);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + (stm - sa));
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc_bf16(128, n, 0, b_mn);
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint64_t ad = make_sdesc(sa + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
+      uint64_t bd;
+      if (b_mn) bd = make_sdesc(sbb + kk * 2048, SLAB, 1024);
+      else bd = make_sdesc(sbb + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
+      umma_bf16(tmem, ad, bd, idesc, kk > 0);
+    }
+    umma_commit(sbar);
+  }
+  __syncwarp();
+  mbar_wait(sbar, 0);
+  tc_fence_after();
+  const int row = warp * 32 + (threadIdx.x & 31);
+  for (int c = 0; c < n; c += 32) {
+    float v[32];
+    tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c, v);
+    tmem_wait_ld();
+    for (int i = 0; i < 32; ++i) d[row * n + c + i] = v[i];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
+}  // namespace
+
+int launch_selftest_umma(const void* a, const void* b, float* d, int n, int b_mn_major,
+                         cudaStream_t stream) {
+  const int smem = 4 * SLAB + 64 + 1024;
+  cudaError_t e =
+      cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(selftest)");
+  selftest_kernel<<<1, 128, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(a),
+                                            reinterpret_cast<const __nv_bfloat16*>(b), d, n,
+                                            b_mn_major);
+  return check_launch("selftest_kernel");
+}
+
+}  // namespace a2d

@@ -1,0 +1,377 @@
+// tile_fwd.cu — Attention2D tile forward on sm_100a.
+//
+// Computes, for one (query tile of 128 rows, head) per CTA, the streaming
+// softmax recurrence of the reference's flash_forward
+// (pkg/src/attn2d/kernels/numpy_backend.py:24-43, numba_backend.py:38-76):
+// S = scale Q K^T over key tiles of 128, running max / denominator, O += P V,
+// causal masking by global token index, rows that see nothing stay empty.
+// It emits the partial state (O normalised, LSE) that the k-way merge
+// (lse_merge.cu) folds across the grid, exactly as attn_fix does
+// (attention.py:194-214).
+//
+// Warp roles (192 threads, one CTA per SM):
+//   warp 0     TMA producer: Q once, then K/V tiles into 2-stage rings
+//   warp 1     tcgen05 MMA issuer (one elected lane) + TMEM owner
+//   warps 2-5  softmax warpgroup: one query row per thread (= TMEM lane)
+// TMEM (512 columns): S double buffer at [0,128) and [128,256), O at 256.
+// S_{j+1} = Q K_{j+1}^T runs on the tensor pipe while the softmax
+// warpgroup turns S_j into P_j; P_j goes to shared memory (bf16, 128B
+// swizzle, K-major) and O += P_j V_j is issued as soon as it lands.
+// The running max is only moved when it grows by more than 2^8 (log2
+// domain), so O in TMEM is rarely rescaled; the final normalisation uses
+// the same stale max for numerator and denominator, which is exact.
+#include "sm100.cuh"
+#include "tiles.cuh"
+#include "kernels.h"
+
+namespace a2d {
+
+namespace {
+
+constexpr int FWD_THREADS = 192;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThreshold = 8.0f;
+
+template <int HD>
+struct FwdLayout {
+  static constexpr int SLAB = TILE * 128;  // bytes of one 128-row x 64-col bf16 slab
+  static constexpr int SLABS = HD / 64;
+  static constexpr int TILE_BYTES = SLAB * SLABS;
+  static constexpr int KST = 2;
+  static constexpr int VST = 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + TILE_BYTES;
+  static constexpr int OFF_V = OFF_K + KST * TILE_BYTES;
+  static constexpr int OFF_P = OFF_V + VST * TILE_BYTES;
+  static constexpr int OFF_BAR = OFF_P + 2 * SLAB;
+  // barriers
+  static constexpr int B_Q = 0;
+  static constexpr int B_KFULL = 1;
+  static constexpr int B_KEMPTY = B_KFULL + KST;
+  static constexpr int B_VFULL = B_KEMPTY + KST;
+  static constexpr int B_VEMPTY = B_VFULL + VST;
+  static constexpr int B_SFULL = B_VEMPTY + VST;
+  static constexpr int B_PFULL = B_SFULL + 2;
+  static constexpr int B_PVDONE = B_PFULL + 1;
+  static constexpr int NBAR = B_PVDONE + 1;
+  static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
+  static constexpr int BYTES = OFF_TMEMPTR + 16;
+  static constexpr int SMEM = BYTES + 1024;  // slack for 1024-B alignment
+};
+
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t TM_S = 0;    // S[b] at b*128
+constexpr uint32_t TM_O = 256;
+
+template <int HD>
+__global__ void __launch_bounds__(FWD_THREADS, 1)
+    fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ a2d_tile_fwd_args p) {
+  using L = FwdLayout<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int bh = blockIdx.x;
+  const int qt_idx = gridDim.y - 1 - blockIdx.y;  // heaviest (causal) tiles first
+  auto bar = [&](int i) { return sb + L::OFF_BAR + 8 * i; };
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(L::B_Q), 1);
+    for (int i = 0; i < L::KST; ++i) {
+      mbar_init(bar(L::B_KFULL + i), 1);
+      mbar_init(bar(L::B_KEMPTY + i), 1);
+    }
+    for (int i = 0; i < L::VST; ++i) {
+      mbar_init(bar(L::B_VFULL + i), 1);
+      mbar_init(bar(L::B_VEMPTY + i), 1);
+    }
+    mbar_init(bar(L::B_SFULL + 0), 1);
+    mbar_init(bar(L::B_SFULL + 1), 1);
+    mbar_init(bar(L::B_PFULL), 128);
+    mbar_init(bar(L::B_PVDONE), 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+  }
+  if (warp == 1) {
+    tmem_alloc(sb + L::OFF_TMEMPTR, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + L::OFF_TMEMPTR);
+
+  const bool causal = p.causal != 0;
+  const TileRef qt = tile_ref(p.q_map, p.nq, qt_idx * TILE);
+  TileRange kr;
+  key_range(p.k_map, p.nk, causal, qt.gmax, kr);
+  const int n_tiles = kr.total;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0 && n_tiles > 0) {
+      mbar_expect_tx(bar(L::B_Q), L::TILE_BYTES);
+      for (int s = 0; s < L::SLABS; ++s)
+        tma_load_3d(sb + L::OFF_Q + s * L::SLAB, &tm_q, bar(L::B_Q), s * 64, qt.row0, bh);
+      TileCursor cur;
+      cur.start(kr);
+      int ks = 0, kph = 0, vs = 0, vph = 0;
+      for (int j = 0; j < n_tiles; ++j, cur.next(kr)) {
+        const int krow = cur.row0(p.k_map);
+        mbar_wait(bar(L::B_KEMPTY + ks), kph ^ 1);
+        mbar_expect_tx(bar(L::B_KFULL + ks), L::TILE_BYTES);
+        for (int s = 0; s < L::SLABS; ++s)
+          tma_load_3d(sb + L::OFF_K + ks * L::TILE_BYTES + s * L::SLAB, &tm_k,
+                      bar(L::B_KFULL + ks), s * 64, krow, bh);
+        if (++ks == L::KST) { ks = 0; kph ^= 1; }
+        mbar_wait(bar(L::B_VEMPTY + vs), vph ^ 1);
+        mbar_expect_tx(bar(L::B_VFULL + vs), L::TILE_BYTES);
+        for (int s = 0; s < L::SLABS; ++s)
+          tma_load_3d(sb + L::OFF_V + vs * L::TILE_BYTES + s * L::SLAB, &tm_v,
+                      bar(L::B_VFULL + vs), s * 64, krow, bh);
+        if (++vs == L::VST) { vs = 0; vph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && n_tiles > 0) {
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(128, HD, 0, 1);
+      int ks = 0, kph = 0, vs = 0, vph = 0;
+      mbar_wait(bar(L::B_Q), 0);
+      tc_fence_after();
+      auto issue_qk = [&](int j) {
+        mbar_wait(bar(L::B_KFULL + ks), kph);
+        tc_fence_after();
+        const uint32_t d = tmem + TM_S + (j & 1) * 128;
+        const uint32_t kbase = sb + L::OFF_K + ks * L::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * L::SLAB + (kk & 3) * 32;
+          umma_bf16(d, make_sdesc(sb + L::OFF_Q + off, 16, 1024), make_sdesc(kbase + off, 16, 1024),
+                    idesc_qk, kk > 0);
+        }
+        umma_commit(bar(L::B_KEMPTY + ks));
+        umma_commit(bar(L::B_SFULL + (j & 1)));
+        if (++ks == L::KST) { ks = 0; kph ^= 1; }
+      };
+      issue_qk(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_qk(j + 1);
+        mbar_wait(bar(L::B_PFULL), j & 1);
+        mbar_wait(bar(L::B_VFULL + vs), vph);
+        tc_fence_after();
+        const uint32_t vbase = sb + L::OFF_V + vs * L::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk) {
+          const uint64_t a = make_sdesc(sb + L::OFF_P + (kk >> 2) * L::SLAB + (kk & 3) * 32, 16, 1024);
+          const uint64_t b = make_sdesc(vbase + kk * 2048, L::SLAB, 1024);
+          umma_bf16(tmem + TM_O, a, b, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(bar(L::B_VEMPTY + vs));
+        umma_commit(bar(L::B_PVDONE));
+        if (++vs == L::VST) { vs = 0; vph ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax WG
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+    const float sl2 = p.scale * kLog2e;
+    float m_run = -INFINITY;  // running max of scale*log2e*s
+    float l_run = 0.f;
+    TileCursor cur;
+    cur.start(kr);
+    for (int j = 0; j < n_tiles; ++j, cur.next(kr)) {
+      const TileRef kt = tile_ref(p.k_map, p.nk, cur.row0(p.k_map));
+      const PairMask pm = pair_mask(p.q_map, qt, kt, causal);
+      int lim = TILE - 1;
+      if (pm.partial) lim = row_limit(p.q_map, p.k_map, qt, kt, pm, causal, row);
+
+      mbar_wait(bar(L::B_SFULL + (j & 1)), (j >> 1) & 1);
+      tc_fence_after();
+      float s[TILE];
+#pragma unroll
+      for (int c = 0; c < TILE / 32; ++c)
+        tmem_ld32(tmem + lane_addr + TM_S + (j & 1) * 128 + c * 32, s + c * 32);
+      tmem_wait_ld();
+      if (pm.partial) {
+#pragma unroll
+        for (int jj = 0; jj < TILE; ++jj)
+          if (jj > lim) s[jj] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int jj = 1; jj < TILE; ++jj) mx = fmaxf(mx, s[jj]);
+      const float m_new = fmaxf(m_run, mx * sl2);
+      float alpha = 1.f;
+      if (m_new > m_run + kRescaleThreshold) {
+        alpha = ex2(m_run - m_new);
+        m_run = m_new;
+      }
+      const float mb = (m_run == -INFINITY) ? 0.f : m_run;
+      uint32_t pk[TILE / 2];
+      float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+      for (int jj = 0; jj < TILE; jj += 2) {
+        const float p0 = ex2(fmaf(s[jj], sl2, -mb));
+        const float p1 = ex2(fmaf(s[jj + 1], sl2, -mb));
+        sum0 += p0;
+        sum1 += p1;
+        pk[jj / 2] = pack_bf16(p0, p1);
+      }
+      l_run = l_run * alpha + (sum0 + sum1);
+
+      // P buffer and O are free once PV_{j-1} has completed.
+      if (j > 0) {
+        mbar_wait(bar(L::B_PVDONE), (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            float o[32];
+            tmem_ld32(tmem + lane_addr + TM_O + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            tmem_st32(tmem + lane_addr + TM_O + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+      }
+      // P (bf16) -> shared, K-major 128B-swizzled: row `row`, 16 chunks of 16 B.
+      const uint32_t prow = sb + L::OFF_P + row * 128;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        const uint32_t addr = prow + (cc >> 3) * L::SLAB + (((cc & 7) ^ (row & 7)) << 4);
+        st_shared_v4(addr, pk[cc * 4 + 0], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(bar(L::B_PFULL));
+    }
+
+    // ------------------------------------------------------------ epilogue
+    if (n_tiles > 0) {
+      mbar_wait(bar(L::B_PVDONE), (n_tiles - 1) & 1);
+      tc_fence_after();
+    }
+    const bool valid = row < qt.nvalid;
+    const int grow = qt.row0 + row;
+    const float lse_new = (l_run > 0.f) ? (m_run + lg2(l_run)) * kLn2 : -INFINITY;
+    float w_new = (l_run > 0.f) ? 1.f / l_run : 0.f;
+    float w_old = 0.f;
+    float lse_out = lse_new;
+    float* lse_ptr = p.lse + (long long)bh * p.nq + grow;
+    if (p.accumulate && valid) {
+      const float lse_old = *lse_ptr;
+      const float mxl = fmaxf(lse_old, lse_new);
+      if (mxl == -INFINITY) {
+        w_old = 0.f;
+        w_new = 0.f;
+        lse_out = -INFINITY;
+      } else {
+        const float eo = __expf(lse_old - mxl);
+        const float en = __expf(lse_new - mxl);
+        const float inv = 1.f / (eo + en);
+        w_old = eo * inv;
+        w_new *= en * inv;
+        lse_out = mxl + __logf(eo + en);
+      }
+    }
+    if (valid) *lse_ptr = lse_out;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      float o[32];
+      if (n_tiles > 0) {
+        tmem_ld32(tmem + lane_addr + TM_O + c * 32, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = 0.f;
+      }
+      if (!valid) continue;
+      if (p.o_dtype == A2D_F32) {
+        float* dst = reinterpret_cast<float*>(p.o) + (long long)bh * p.o_stride_bh +
+                     (long long)grow * p.o_stride_row + c * 32;
+        if (p.accumulate) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 old = *reinterpret_cast<const float4*>(dst + i);
+            float4 v;
+            v.x = old.x * w_old + o[i + 0] * w_new;
+            v.y = old.y * w_old + o[i + 1] * w_new;
+            v.z = old.z * w_old + o[i + 2] * w_new;
+            v.w = old.w * w_old + o[i + 3] * w_new;
+            *reinterpret_cast<float4*>(dst + i) = v;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + i) =
+                make_float4(o[i] * w_new, o[i + 1] * w_new, o[i + 2] * w_new, o[i + 3] * w_new);
+        }
+      } else {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) +
+                             (long long)bh * p.o_stride_bh + (long long)grow * p.o_stride_row +
+                             c * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 v;
+          v.x = pack_bf16(o[i + 0] * w_new, o[i + 1] * w_new);
+          v.y = pack_bf16(o[i + 2] * w_new, o[i + 3] * w_new);
+          v.z = pack_bf16(o[i + 4] * w_new, o[i + 5] * w_new);
+          v.w = pack_bf16(o[i + 6] * w_new, o[i + 7] * w_new);
+          *reinterpret_cast<uint4*>(dst + i) = v;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+}  // namespace
+
+template <int HD>
+int launch_fwd_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                  const CUtensorMap& tv, cudaStream_t stream) {
+  using L = FwdLayout<HD>;
+  static bool configured[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!configured[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         L::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fwd)");
+    configured[dev & 63] = true;
+  }
+  const int q_tiles = (a.q_map.mode == A2D_IDX_AFFINE && a.q_map.nblocks > 1)
+                          ? a.q_map.nblocks * (a.q_map.rows_per_block / TILE)
+                          : (a.nq + TILE - 1) / TILE;
+  dim3 grid(a.bh, q_tiles);
+  fwd_kernel<HD><<<grid, FWD_THREADS, L::SMEM, stream>>>(tq, tk, tv, a);
+  return check_launch("fwd_kernel");
+}
+
+int launch_tile_fwd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                    const CUtensorMap& tv, cudaStream_t stream) {
+  if (a.h == 128) return launch_fwd_hd<128>(a, tq, tk, tv, stream);
+  return launch_fwd_hd<64>(a, tq, tk, tv, stream);
+}
+
+}  // namespace a2d

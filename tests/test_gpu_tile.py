@@ -1,0 +1,166 @@
+"""GPU parity of the sm_100a tile kernels against the reference's own
+outputs (golden fixtures from the unmodified reference) and against a torch
+fp32 restatement at larger sizes.  Tolerances: rel-Fro
+<= 1e-2 on O/dQ/dK/dV, LSE max-abs <= 1e-3 — bf16 inputs and P, fp32
+accumulation vs the fp64 reference."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_util import bf16_from_bits, max_abs, ref_attention, rel_fro, uniform
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+REL_TOL = 1e-2
+LSE_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2503_15758_b200 import ops as _ops
+    return _ops
+
+
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("n", [64, 128])
+def test_umma_descriptor_selftest(ops, b_mn, n):
+    a = uniform((128, 128), 1)
+    b = uniform((128, n) if b_mn else (n, 128), 2)
+    d = ops.selftest_umma(a, b, b_mn)
+    want = a.float() @ (b.float() if b_mn else b.float().T)
+    torch.cuda.synchronize()
+    assert max_abs(d, want) < 1e-3, max_abs(d, want)
+
+
+GOLD_CASES = ["n256_h64_causal", "n256_h64_none_s1", "n128_h128_causal", "n320_h128_none"]
+
+
+@pytest.mark.parametrize("tag", GOLD_CASES)
+def test_forward_matches_reference_golden(ops, tag):
+    g = np.load(GOLD / "gpu_parity.npz")
+    n, h, causal, scale = g[f"{tag}_meta"]
+    q, k, v = (bf16_from_bits(g[f"{tag}_{x}"]).cuda()[None] for x in "qkv")
+    o, lse = ops.tile_forward(q, k, v, causal=bool(causal), scale=float(scale))
+    want_o = torch.from_numpy(g[f"{tag}_o"]).cuda()
+    want_lse = torch.from_numpy(g[f"{tag}_lse"]).cuda()
+    assert rel_fro(o[0], want_o) < REL_TOL
+    assert max_abs(lse[0], want_lse) < LSE_TOL
+    ob, lse2 = ops.tile_forward(q, k, v, causal=bool(causal), scale=float(scale),
+                                out_dtype=torch.bfloat16)
+    assert rel_fro(ob[0].float(), want_o) < REL_TOL
+    assert torch.equal(lse, lse2)
+
+
+@pytest.mark.parametrize("h", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("nq,nk", [(128, 128), (200, 200), (1024, 1024), (384, 1000), (7, 9)])
+def test_forward_vs_torch(ops, h, causal, nq, nk):
+    bh = 3
+    q, k, v = uniform((bh, nq, h), 10), uniform((bh, nk, h), 11), uniform((bh, nk, h), 12)
+    scale = h ** -0.5
+    # causal with nq != nk: queries are the LAST nq positions of the key range
+    qi = ops.TokenIndex.contiguous(nq, start=max(nk - nq, 0))
+    o, lse = ops.tile_forward(q, k, v, causal=causal, scale=scale, q_index=qi)
+    q_idx = torch.arange(nq) + max(nk - nq, 0)
+    want_o, want_lse = ref_attention(q, k, v, causal, scale, q_idx=q_idx)
+    torch.cuda.synchronize()
+    assert rel_fro(o, want_o) < REL_TOL
+    fin = torch.isfinite(want_lse)
+    assert torch.equal(fin, torch.isfinite(lse))
+    assert max_abs(lse[fin], want_lse[fin]) < LSE_TOL
+
+
+def test_forward_unit_scale_peaky(ops):
+    """Reference default scale = 1.0 (common.py:26): large scores."""
+    q, k, v = uniform((2, 512, 128), 20), uniform((2, 512, 128), 21), uniform((2, 512, 128), 22)
+    o, lse = ops.tile_forward(q, k, v, causal=True, scale=1.0)
+    want_o, want_lse = ref_attention(q, k, v, True, 1.0)
+    assert rel_fro(o, want_o) < REL_TOL
+    assert max_abs(lse, want_lse) < LSE_TOL
+
+
+def test_forward_index_subsets_array_mode(ops):
+    """Global indices drive masking, not local positions
+    (reference test_attention.py:136-145), incl. fully masked rows."""
+    rng = np.random.default_rng(5)
+    q_idx = np.sort(rng.choice(600, size=150, replace=False))
+    k_idx = np.sort(rng.choice(np.arange(20, 600), size=260, replace=False))
+    qi = ops.TokenIndex.from_indices(q_idx)
+    ki = ops.TokenIndex.from_indices(k_idx)
+    assert qi.is_array and ki.is_array
+    q, k, v = uniform((2, 150, 64), 30), uniform((2, 260, 64), 31), uniform((2, 260, 64), 32)
+    o, lse = ops.tile_forward(q, k, v, causal=True, scale=0.125, q_index=qi, k_index=ki)
+    want_o, want_lse = ref_attention(q, k, v, True, 0.125, torch.from_numpy(q_idx),
+                                     torch.from_numpy(k_idx))
+    empty = q_idx < k_idx[0]
+    assert empty.any()
+    assert torch.all(torch.isneginf(lse[:, torch.from_numpy(empty)]))
+    assert torch.all(o[:, torch.from_numpy(empty)] == 0)
+    live = torch.from_numpy(~empty)
+    assert rel_fro(o[:, live], want_o[:, live]) < REL_TOL
+    assert max_abs(lse[:, live], want_lse[:, live]) < LSE_TOL
+
+
+@pytest.mark.parametrize("pr,pc", [(2, 2), (2, 4), (4, 2)])
+def test_forward_blocked_cyclic_maps(ops, pr, pc):
+    """The 2D gathered orders: query block c' holds tokens r + Pr c' + P i,
+    key block r' holds c + Pc r' + P i."""
+    P, L, h = pr * pc, 256, 128
+    N = P * L
+    r, c = pr - 1, 0
+    qi = ops.TokenIndex.blocked([r + pr * cc for cc in range(pc)], P, L)
+    ki = ops.TokenIndex.blocked([c + pc * rr for rr in range(pr)], P, L)
+    q, k, v = uniform((2, pc * L, h), 40), uniform((2, pr * L, h), 41), uniform((2, pr * L, h), 42)
+    o, lse = ops.tile_forward(q, k, v, causal=True, scale=h ** -0.5, q_index=qi, k_index=ki)
+    want_o, want_lse = ref_attention(q, k, v, True, h ** -0.5, torch.from_numpy(qi.host()),
+                                     torch.from_numpy(ki.host()))
+    fin = torch.isfinite(want_lse)
+    assert torch.equal(fin, torch.isfinite(lse))
+    assert rel_fro(o[fin], want_o[fin]) < REL_TOL
+    assert max_abs(lse[fin], want_lse[fin]) < LSE_TOL
+    # the same maps through the array path agree
+    o2, lse2 = ops.tile_forward(q, k, v, causal=True, scale=h ** -0.5, q_index=qi.as_array("cuda"),
+                                k_index=ki.as_array("cuda"))
+    assert max_abs(o2, o) < 1e-5 and max_abs(lse2[fin], lse[fin]) < 1e-5
+
+
+def test_forward_continuation(ops):
+    """Two calls over split key ranges equal one call
+    (reference test_kernels.py:124-137)."""
+    q, k, v = uniform((2, 300, 128), 50), uniform((2, 700, 128), 51), uniform((2, 700, 128), 52)
+    qi = ops.TokenIndex.contiguous(300, start=400)
+    whole_o, whole_lse = ops.tile_forward(q, k, v, causal=True, scale=0.1, q_index=qi)
+    o, lse = ops.tile_forward(q, k[:, :256], v[:, :256], causal=True, scale=0.1, q_index=qi,
+                              k_index=ops.TokenIndex.contiguous(256))
+    ops.tile_forward(q, k[:, 256:], v[:, 256:], causal=True, scale=0.1, q_index=qi,
+                     k_index=ops.TokenIndex.contiguous(444, start=256), out=o, lse=lse,
+                     accumulate=True)
+    assert max_abs(o, whole_o) < 1e-3
+    assert max_abs(lse, whole_lse) < 1e-3
+
+
+@pytest.mark.parametrize("kparts", [1, 2, 4, 8])
+def test_lse_merge_matches_oracle(ops, kparts):
+    import sys
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from oracle import attn2d_oracle as orc
+    rows, h = 333, 128
+    g = torch.Generator().manual_seed(kparts)
+    o_parts = torch.randn((kparts, rows, h), generator=g)
+    lse_parts = torch.randn((kparts, rows), generator=g) * 3
+    lse_parts[0, :5] = float("-inf")
+    if kparts > 1:
+        lse_parts[:, 7] = float("-inf")
+    o, lse = ops.lse_merge(o_parts.cuda(), lse_parts.cuda(), out_dtype=torch.float32)
+    want_o, want_lse = orc.lse_merge(list(o_parts.double().numpy()),
+                                     list(lse_parts.double().numpy()))
+    assert np.abs(o.cpu().numpy() - want_o).max() < 1e-5
+    fin = np.isfinite(want_lse)
+    assert np.array_equal(fin, np.isfinite(lse.cpu().numpy()))
+    assert np.abs(lse.cpu().numpy()[fin] - want_lse[fin]).max() < 1e-5
