@@ -56,7 +56,7 @@ EncodeTiledFn encode_fn() {
 // 3-D map over a bf16 [bh, rows, h] tensor (unit stride along h), box 64 x 128 x 1,
 // 128-byte swizzle: one box is one K-major SW128 slab of a 128-row tile.
 int make_map(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long long s_row,
-             long long s_bh, const char* name) {
+             long long s_bh, const char* name, int box_rows = 128) {
   if (ptr == nullptr) return set_error(A2D_EINVAL, "%s is null", name);
   if (reinterpret_cast<uintptr_t>(ptr) % 16)
     return set_error(A2D_EINVAL, "%s must be 16-byte aligned", name);
@@ -67,7 +67,7 @@ int make_map(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long long
   cuuint64_t dims[3] = {(cuuint64_t)h, (cuuint64_t)rows, (cuuint64_t)bh};
   cuuint64_t strides[2] = {(cuuint64_t)(s_row * 2), (cuuint64_t)(s_bh * 2)};
   if (bh == 1) strides[1] = (cuuint64_t)((long long)rows * s_row * 2);
-  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -75,6 +75,27 @@ int make_map(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long long
   if (r != CUDA_SUCCESS) return set_error(A2D_ECUDA, "cuTensorMapEncodeTiled(%s) failed: %d", name, (int)r);
   return A2D_OK;
 }
+
+}  // namespace
+
+// fp32 [bh, rows, h] contiguous accumulator, box 32 x box_rows x 1, 128B swizzle
+// (the backward's dQ reduce-add target).
+int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, int box_rows) {
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) return set_error(A2D_EINVAL, "dq_acc must be 16-byte aligned");
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return set_error(A2D_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)h, (cuuint64_t)rows, (cuuint64_t)bh};
+  cuuint64_t strides[2] = {(cuuint64_t)h * 4, (cuuint64_t)h * 4 * rows};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(A2D_ECUDA, "cuTensorMapEncodeTiled(dq_acc) failed: %d", (int)r);
+  return A2D_OK;
+}
+
+namespace {
 
 int check_map(const a2d_index_map& m, int n, const char* name) {
   if (m.mode == A2D_IDX_ARRAY) {
@@ -169,10 +190,12 @@ int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
     return set_error(A2D_EINVAL, "null output / statistics pointer");
   if (a->bh == 0 || a->nk == 0) return A2D_OK;
   CUtensorMap tq, tk, tv, tdo;
-  if ((rc = make_map(&tq, a->q, a->h, a->nq, a->bh, a->q_stride_row, a->q_stride_bh, "q"))) return rc;
+  const int qt = bwd_q_tile_rows(a->h);
+  if ((rc = make_map(&tq, a->q, a->h, a->nq, a->bh, a->q_stride_row, a->q_stride_bh, "q", qt))) return rc;
   if ((rc = make_map(&tk, a->k, a->h, a->nk, a->bh, a->k_stride_row, a->k_stride_bh, "k"))) return rc;
   if ((rc = make_map(&tv, a->v, a->h, a->nk, a->bh, a->v_stride_row, a->v_stride_bh, "v"))) return rc;
-  if ((rc = make_map(&tdo, a->dout, a->h, a->nq, a->bh, a->do_stride_row, a->do_stride_bh, "dout")))
+  if ((rc = make_map(&tdo, a->dout, a->h, a->nq, a->bh, a->do_stride_row, a->do_stride_bh, "dout",
+                     qt)))
     return rc;
   return launch_tile_bwd(*a, tq, tk, tv, tdo, static_cast<cudaStream_t>(stream));
 }

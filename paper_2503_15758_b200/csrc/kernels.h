@@ -24,6 +24,8 @@ int launch_bwd_preprocess(const void* o, const void* dout, float* delta, long lo
                           int h, cudaStream_t stream);
 int launch_bwd_finalize(const float* dq_acc, void* dq, int out_dtype, long long sbh,
                         long long srow, int bh, int n, int h, float scale, cudaStream_t stream);
+int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, int box_rows);
+int bwd_q_tile_rows(int h);
 int launch_selftest_umma(const void* a, const void* b, float* d, int n, int b_mn_major,
                          cudaStream_t stream);
 

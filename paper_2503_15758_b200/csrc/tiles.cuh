@@ -49,7 +49,8 @@ struct TileRef {
   long long gmax;  // global index of the last valid row
 };
 
-__device__ __forceinline__ TileRef tile_ref(const a2d_index_map& m, int n, int t_flat_row0) {
+__device__ __forceinline__ TileRef tile_ref(const a2d_index_map& m, int n, int t_flat_row0,
+                                           int T = TILE) {
   TileRef r;
   r.row0 = t_flat_row0;
   int end;
@@ -59,7 +60,7 @@ __device__ __forceinline__ TileRef tile_ref(const a2d_index_map& m, int n, int t
     const int b = t_flat_row0 / m.rows_per_block;
     end = (b + 1) * m.rows_per_block;
   }
-  r.nvalid = min(TILE, end - t_flat_row0);
+  r.nvalid = min(T, end - t_flat_row0);
   r.gmin = gidx(m, t_flat_row0);
   r.gmax = gidx(m, t_flat_row0 + r.nvalid - 1);
   return r;
@@ -109,12 +110,12 @@ __device__ __forceinline__ void key_range(const a2d_index_map& km, int nk, bool 
 
 // Query tiles that attend a key tile whose first global index is kmin.
 __device__ __forceinline__ void query_range(const a2d_index_map& qm, int nq, bool causal,
-                                            long long kmin, TileRange& r) {
+                                            long long kmin, TileRange& r, int T = TILE) {
   r.total = 0;
   r.nblk = (qm.mode == A2D_IDX_ARRAY) ? 1 : qm.nblocks;
   for (int b = 0; b < r.nblk; ++b) {
     const int rows = (qm.mode == A2D_IDX_ARRAY) ? nq : blk_rows(qm, nq, b);
-    const int ntiles = (rows + TILE - 1) / TILE;
+    const int ntiles = (rows + T - 1) / T;
     int first = 0;
     if (causal) {
       if (qm.mode == A2D_IDX_ARRAY) {
@@ -122,19 +123,19 @@ __device__ __forceinline__ void query_range(const a2d_index_map& qm, int nq, boo
         int lo = 0, hi = ntiles;
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          const int lastrow = min(rows, (mid + 1) * TILE) - 1;
+          const int lastrow = min(rows, (mid + 1) * T) - 1;
           if (qm.idx[lastrow] < kmin) lo = mid + 1; else hi = mid;
         }
         first = lo;
       } else {
         const long long base = qm.base[b];
         const long long s = qm.stride;
-        // tile t covers base + s*(128t .. 128t+127); need its max >= kmin
-        const long long need = kmin - base - s * (TILE - 1);
-        first = need <= 0 ? 0 : (int)min((long long)ntiles, ceil_div_s(need, s * TILE));
+        // tile t covers base + s*(T t .. T t + T-1); need its max >= kmin
+        const long long need = kmin - base - s * (T - 1);
+        first = need <= 0 ? 0 : (int)min((long long)ntiles, ceil_div_s(need, s * T));
         // a short tail tile has a smaller maximum than the formula assumes
         if (first < ntiles) {
-          const int lastrow = min(rows, (first + 1) * TILE) - 1;
+          const int lastrow = min(rows, (first + 1) * T) - 1;
           if (base + s * lastrow < kmin) first += 1;
         }
       }
@@ -163,9 +164,9 @@ struct TileCursor {
     ++t;
     skip(r);
   }
-  __device__ __forceinline__ int row0(const a2d_index_map& m) const {
+  __device__ __forceinline__ int row0(const a2d_index_map& m, int T = TILE) const {
     const int rpb = (m.mode == A2D_IDX_ARRAY || m.nblocks == 1) ? 0 : m.rows_per_block;
-    return b * rpb + t * TILE;
+    return b * rpb + t * T;
   }
 };
 

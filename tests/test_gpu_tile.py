@@ -164,3 +164,90 @@ def test_lse_merge_matches_oracle(ops, kparts):
     fin = np.isfinite(want_lse)
     assert np.array_equal(fin, np.isfinite(lse.cpu().numpy()))
     assert np.abs(lse.cpu().numpy()[fin] - want_lse[fin]).max() < 1e-5
+
+
+# --------------------------------------------------------------------------
+# backward
+# --------------------------------------------------------------------------
+
+def _run_backward(ops, q, k, v, dout, causal, scale, q_index=None, k_index=None):
+    o, lse = ops.tile_forward(q, k, v, causal=causal, scale=scale, q_index=q_index,
+                              k_index=k_index, out_dtype=torch.bfloat16)
+    delta = ops.bwd_preprocess(o, dout)
+    dq_acc, dk, dv = ops.tile_backward(q, k, v, dout, lse, delta, causal=causal, scale=scale,
+                                       q_index=q_index, k_index=k_index)
+    dq = ops.bwd_finalize(dq_acc, scale, dtype=torch.float32)
+    return o, lse, dq, dk, dv
+
+
+@pytest.mark.parametrize("tag", GOLD_CASES)
+def test_backward_matches_reference_golden(ops, tag):
+    g = np.load(GOLD / "gpu_parity.npz")
+    n, h, causal, scale = g[f"{tag}_meta"]
+    q, k, v, dout = (bf16_from_bits(g[f"{tag}_{x}"]).cuda()[None] for x in ("q", "k", "v", "dout"))
+    _, _, dq, dk, dv = _run_backward(ops, q, k, v, dout, bool(causal), float(scale))
+    for name, got in (("dq", dq), ("dk", dk), ("dv", dv)):
+        want = torch.from_numpy(g[f"{tag}_{name}"]).cuda()
+        assert rel_fro(got[0], want) < REL_TOL, (name, rel_fro(got[0], want))
+
+
+@pytest.mark.parametrize("h", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("n", [128, 200, 1024])
+def test_backward_vs_torch(ops, h, causal, n):
+    from gpu_util import ref_attention_grad
+    bh = 3
+    q, k, v, dout = (uniform((bh, n, h), 60 + i) for i in range(4))
+    scale = h ** -0.5
+    _, _, dq, dk, dv = _run_backward(ops, q, k, v, dout, causal, scale)
+    wq, wk, wv = ref_attention_grad(q, k, v, dout, causal, scale)
+    torch.cuda.synchronize()
+    for name, got, want in (("dq", dq, wq), ("dk", dk, wk), ("dv", dv, wv)):
+        assert rel_fro(got, want) < REL_TOL, (name, rel_fro(got, want))
+
+
+def test_backward_key_subsets_are_partial_sums(ops):
+    """Key-subset calls with global statistics sum to the full gradient
+    (reference test_attention.py:305-328)."""
+    n, h = 512, 128
+    q, k, v, dout = (uniform((2, n, h), 70 + i) for i in range(4))
+    scale = h ** -0.5
+    o, lse, dq, dk, dv = _run_backward(ops, q, k, v, dout, True, scale)
+    delta = ops.bwd_preprocess(o, dout)
+    dq_acc = torch.zeros((2, n, h), device="cuda")
+    dks, dvs = [], []
+    for lo, hi in ((0, 256), (256, 512)):
+        _, dk_p, dv_p = ops.tile_backward(q, k[:, lo:hi], v[:, lo:hi], dout, lse, delta,
+                                          causal=True, scale=scale, dq_acc=dq_acc,
+                                          k_index=ops.TokenIndex.contiguous(hi - lo, start=lo))
+        dks.append(dk_p)
+        dvs.append(dv_p)
+    dq2 = ops.bwd_finalize(dq_acc, scale, dtype=torch.float32)
+    assert max_abs(dq2, dq) < 1e-4
+    assert max_abs(torch.cat(dks, 1), dk) < 1e-4
+    assert max_abs(torch.cat(dvs, 1), dv) < 1e-4
+
+
+@pytest.mark.parametrize("pr,pc", [(2, 2), (2, 4)])
+def test_backward_blocked_cyclic_maps(ops, pr, pc):
+    from gpu_util import ref_attention
+    P, L, h = pr * pc, 256, 128
+    r, c = 1, pc - 1
+    qi = ops.TokenIndex.blocked([r + pr * cc for cc in range(pc)], P, L)
+    ki = ops.TokenIndex.blocked([c + pc * rr for rr in range(pr)], P, L)
+    q, k, v = uniform((1, pc * L, h), 80), uniform((1, pr * L, h), 81), uniform((1, pr * L, h), 82)
+    dout = uniform((1, pc * L, h), 83)
+    scale = h ** -0.5
+    qi_t, ki_t = torch.from_numpy(qi.host()), torch.from_numpy(ki.host())
+    # global statistics of these query rows against THESE keys only (a tile of
+    # the grid), then the gradient of that partial attention
+    qf = q.float().requires_grad_(True)
+    kf = k.float().requires_grad_(True)
+    vf = v.float().requires_grad_(True)
+    o_ref, lse_ref = ref_attention(qf, kf, vf, True, scale, qi_t, ki_t)
+    live = torch.isfinite(lse_ref)
+    (o_ref * dout.float() * live[..., None]).sum().backward()
+    _, _, dq, dk, dv = _run_backward(ops, q, k, v, dout * live[..., None], True, scale, qi, ki)
+    assert rel_fro(dq[live], qf.grad[live]) < REL_TOL
+    assert rel_fro(dk, kf.grad) < REL_TOL
+    assert rel_fro(dv, vf.grad) < REL_TOL
