@@ -107,7 +107,8 @@ int a2d_bwd_preprocess(const void* o, const void* dout, float* delta,
  * numpy_backend.py:46-62).  lse / delta are the GLOBAL row statistics of q's
  * rows (after every merge), so the gradients are exact partial sums over
  * this key subset (attention.py:225-257).
- *   dq_acc [bh, nq, h] fp32: dS K (unscaled) is ADDED to it (caller zeroes);
+ *   dq_acc [bh, nq, h] fp32 (strides dq_stride_*, multiples of 4 elements):
+ *   dS K (unscaled) is ADDED to it with TMA reduce-add (caller zeroes);
  *   dk, dv [bh, nk, h]: written (dkv_dtype A2D_F32 or A2D_BF16); dk is
  *   already multiplied by scale. */
 typedef struct {
@@ -124,6 +125,7 @@ typedef struct {
   int64_t k_stride_bh, k_stride_row;
   int64_t v_stride_bh, v_stride_row;
   int64_t do_stride_bh, do_stride_row;
+  int64_t dq_stride_bh, dq_stride_row;
   int64_t dkv_stride_bh, dkv_stride_row;
   int32_t bh, nq, nk, h;
   int32_t causal;
@@ -136,9 +138,10 @@ typedef struct {
 
 int a2d_tile_bwd(const a2d_tile_bwd_args* args, void* stream);
 
-/* dq = scale * dq_acc, converted to out_dtype ([bh, n, h], given strides). */
-int a2d_bwd_finalize(const float* dq_acc, void* dq, int32_t out_dtype,
-                     int64_t dq_stride_bh, int64_t dq_stride_row,
+/* dq = scale * dq_acc, converted to out_dtype; both [bh, n, h] with the
+ * given strides (unit stride along h). */
+int a2d_bwd_finalize(const float* dq_acc, int64_t acc_stride_bh, int64_t acc_stride_row,
+                     void* dq, int32_t out_dtype, int64_t dq_stride_bh, int64_t dq_stride_row,
                      int32_t bh, int32_t n, int32_t h, float scale, void* stream);
 
 /* k-way log-sum-exp merge of partial (O, LSE) over disjoint key sets —

@@ -54,6 +54,7 @@ class TileBwdArgs(ctypes.Structure):
                 ("k_stride_bh", c_int64), ("k_stride_row", c_int64),
                 ("v_stride_bh", c_int64), ("v_stride_row", c_int64),
                 ("do_stride_bh", c_int64), ("do_stride_row", c_int64),
+                ("dq_stride_bh", c_int64), ("dq_stride_row", c_int64),
                 ("dkv_stride_bh", c_int64), ("dkv_stride_row", c_int64),
                 ("bh", c_int32), ("nq", c_int32), ("nk", c_int32), ("h", c_int32),
                 ("causal", c_int32), ("scale", c_float), ("dkv_dtype", c_int32),
@@ -78,8 +79,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     lib.a2d_tile_bwd.argtypes = [ctypes.POINTER(TileBwdArgs), c_void_p]
     lib.a2d_bwd_preprocess.argtypes = [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
                                        c_int64, c_int32, c_int32, c_int32, c_void_p]
-    lib.a2d_bwd_finalize.argtypes = [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int32,
-                                     c_int32, c_int32, c_float, c_void_p]
+    lib.a2d_bwd_finalize.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64,
+                                     c_int64, c_int32, c_int32, c_int32, c_float, c_void_p]
     lib.a2d_lse_merge.argtypes = [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int64,
                                   c_int32, c_int64, c_void_p, c_int32, c_int64, c_void_p,
                                   c_void_p]

@@ -80,12 +80,16 @@ int make_map(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long long
 
 // fp32 [bh, rows, h] contiguous accumulator, box 32 x box_rows x 1, 128B swizzle
 // (the backward's dQ reduce-add target).
-int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, int box_rows) {
+int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, long long s_row,
+                    long long s_bh, int box_rows) {
   if (reinterpret_cast<uintptr_t>(ptr) % 16) return set_error(A2D_EINVAL, "dq_acc must be 16-byte aligned");
+  if ((s_row * 4) % 16 || (s_bh * 4) % 16)
+    return set_error(A2D_EINVAL, "dq_acc strides must be multiples of 4 elements");
   EncodeTiledFn fn = encode_fn();
   if (!fn) return set_error(A2D_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)h, (cuuint64_t)rows, (cuuint64_t)bh};
-  cuuint64_t strides[2] = {(cuuint64_t)h * 4, (cuuint64_t)h * 4 * rows};
+  cuuint64_t strides[2] = {(cuuint64_t)(s_row * 4), (cuuint64_t)(s_bh * 4)};
+  if (bh == 1) strides[1] = (cuuint64_t)((long long)rows * s_row * 4);
   cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box,
@@ -200,13 +204,15 @@ int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
   return launch_tile_bwd(*a, tq, tk, tv, tdo, static_cast<cudaStream_t>(stream));
 }
 
-int a2d_bwd_finalize(const float* dq_acc, void* dq, int32_t out_dtype, int64_t dq_stride_bh,
-                     int64_t dq_stride_row, int32_t bh, int32_t n, int32_t h, float scale,
-                     void* stream) {
+int a2d_bwd_finalize(const float* dq_acc, int64_t acc_stride_bh, int64_t acc_stride_row, void* dq,
+                     int32_t out_dtype, int64_t dq_stride_bh, int64_t dq_stride_row, int32_t bh,
+                     int32_t n, int32_t h, float scale, void* stream) {
   if (!dq_acc || !dq) return set_error(A2D_EINVAL, "null pointer");
-  if (h % 4) return set_error(A2D_EINVAL, "h must be a multiple of 4");
-  return launch_bwd_finalize(dq_acc, dq, out_dtype, dq_stride_bh, dq_stride_row, bh, n, h, scale,
-                             static_cast<cudaStream_t>(stream));
+  if (h % 4 || acc_stride_bh % 4 || acc_stride_row % 4 || dq_stride_bh % 4 || dq_stride_row % 4)
+    return set_error(A2D_EINVAL, "h and strides must be multiples of 4");
+  if (out_dtype != A2D_F32 && out_dtype != A2D_BF16) return set_error(A2D_EINVAL, "out_dtype invalid");
+  return launch_bwd_finalize(dq_acc, acc_stride_bh, acc_stride_row, dq, out_dtype, dq_stride_bh,
+                             dq_stride_row, bh, n, h, scale, static_cast<cudaStream_t>(stream));
 }
 
 int a2d_lse_merge(const float* o_parts, const float* lse_parts, int32_t k_parts,

@@ -22,9 +22,11 @@ int launch_lse_merge(const float* o_parts, const float* lse_parts, int k_parts,
 int launch_bwd_preprocess(const void* o, const void* dout, float* delta, long long o_sbh,
                           long long o_srow, long long do_sbh, long long do_srow, int bh, int n,
                           int h, cudaStream_t stream);
-int launch_bwd_finalize(const float* dq_acc, void* dq, int out_dtype, long long sbh,
-                        long long srow, int bh, int n, int h, float scale, cudaStream_t stream);
-int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, int box_rows);
+int launch_bwd_finalize(const float* dq_acc, long long asbh, long long asrow, void* dq,
+                        int out_dtype, long long sbh, long long srow, int bh, int n, int h,
+                        float scale, cudaStream_t stream);
+int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, long long s_row,
+                    long long s_bh, int box_rows);
 int bwd_q_tile_rows(int h);
 int launch_selftest_umma(const void* a, const void* b, float* d, int n, int b_mn_major,
                          cudaStream_t stream);

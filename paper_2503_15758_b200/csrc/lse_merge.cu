@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
 }
 
 __global__ void __launch_bounds__(256) bwd_finalize_kernel(const float* __restrict__ acc,
+                                                           long long asbh, long long asrow,
                                                            void* __restrict__ dq, int out_dtype,
                                                            long long sbh, long long srow, int bh,
                                                            int n, int h, float scale) {
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(256) bwd_finalize_kernel(const float* __restri
     const long long rr = e / h;
     const int r = (int)(rr % n);
     const int b = (int)(rr / n);
-    float4 v = *reinterpret_cast<const float4*>(acc + e);
+    float4 v = *reinterpret_cast<const float4*>(acc + b * asbh + (long long)r * asrow + c);
     v.x *= scale; v.y *= scale; v.z *= scale; v.w *= scale;
     const long long dst = b * sbh + (long long)r * srow + c;
     if (out_dtype == A2D_F32) {
@@ -153,14 +154,15 @@ int launch_bwd_preprocess(const void* o, const void* dout, float* delta, long lo
   return check_launch("bwd_preprocess_kernel");
 }
 
-int launch_bwd_finalize(const float* dq_acc, void* dq, int out_dtype, long long sbh,
-                        long long srow, int bh, int n, int h, float scale, cudaStream_t stream) {
+int launch_bwd_finalize(const float* dq_acc, long long asbh, long long asrow, void* dq,
+                        int out_dtype, long long sbh, long long srow, int bh, int n, int h,
+                        float scale, cudaStream_t stream) {
   const long long total4 = (long long)bh * n * h / 4;
   if (total4 == 0) return A2D_OK;
   long long blocks = (total4 + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  bwd_finalize_kernel<<<(unsigned)blocks, 256, 0, stream>>>(dq_acc, dq, out_dtype, sbh, srow, bh,
-                                                            n, h, scale);
+  bwd_finalize_kernel<<<(unsigned)blocks, 256, 0, stream>>>(dq_acc, asbh, asrow, dq, out_dtype,
+                                                            sbh, srow, bh, n, h, scale);
   return check_launch("bwd_finalize_kernel");
 }
 

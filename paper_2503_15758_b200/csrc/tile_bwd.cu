@@ -474,7 +474,7 @@ int launch_bwd_hd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUten
     configured[dev & 63] = true;
   }
   CUtensorMap tdq;
-  int rc = make_map_f32_dq(&tdq, a.dq_acc, HD, a.nq, a.bh, L::QT);
+  int rc = make_map_f32_dq(&tdq, a.dq_acc, HD, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh, L::QT);
   if (rc) return rc;
   const int k_tiles = (a.k_map.mode == A2D_IDX_AFFINE && a.k_map.nblocks > 1)
                           ? a.k_map.nblocks * (a.k_map.rows_per_block / TILE)

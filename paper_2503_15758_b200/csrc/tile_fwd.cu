@@ -75,8 +75,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   const uint32_t sb = smem_u32(smem);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int bh = blockIdx.x;
-  const int qt_idx = gridDim.y - 1 - blockIdx.y;  // heaviest (causal) tiles first
+  // q tiles vary fastest so co-resident CTAs share one head's K/V in L2;
+  // within a head the heaviest (causal) tiles start first.
+  const int bh = blockIdx.y;
+  const int qt_idx = gridDim.x - 1 - blockIdx.x;
   auto bar = [&](int i) { return sb + L::OFF_BAR + 8 * i; };
 
   if (threadIdx.x == 0) {
@@ -363,7 +365,7 @@ int launch_fwd_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUten
   const int q_tiles = (a.q_map.mode == A2D_IDX_AFFINE && a.q_map.nblocks > 1)
                           ? a.q_map.nblocks * (a.q_map.rows_per_block / TILE)
                           : (a.nq + TILE - 1) / TILE;
-  dim3 grid(a.bh, q_tiles);
+  dim3 grid(q_tiles, a.bh);
   fwd_kernel<HD><<<grid, FWD_THREADS, L::SMEM, stream>>>(tq, tk, tv, a);
   return check_launch("fwd_kernel");
 }

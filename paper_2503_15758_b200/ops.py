@@ -59,10 +59,11 @@ class TokenIndex:
         d = np.diff(host)
         if np.all(d == d[0]) and d[0] >= 1:
             return cls(n=n, bases=(int(host[0]),), stride=int(d[0]), rows_per_block=n, _host=host)
-        # blocks of 128*k rows sharing a stride
-        for rpb in range(128, n // 2 + 1, 128):
-            if n % rpb or n // rpb > _lib.MAX_BLOCKS:
+        # fewest blocks of 128*k rows sharing a stride
+        for nb in range(2, _lib.MAX_BLOCKS + 1):
+            if n % nb or (n // nb) % 128:
                 continue
+            rpb = n // nb
             blk = host.reshape(n // rpb, rpb)
             dd = np.diff(blk, axis=1)
             if np.all(dd == dd[0, 0]) and dd[0, 0] >= 1:
@@ -251,8 +252,8 @@ def tile_backward(q, k, v, dout, lse, delta, *, causal: bool, scale: float,
         dk = torch.empty((bh, nk, h), dtype=dkv_dtype, device=q.device)
     if dv is None:
         dv = torch.empty((bh, nk, h), dtype=dkv_dtype, device=q.device)
-    if not dq_acc.is_contiguous() or dq_acc.dtype != torch.float32:
-        raise ShapeError("dq_acc must be contiguous fp32")
+    if dq_acc.dtype != torch.float32 or dq_acc.shape != (bh, nq, h) or dq_acc.stride(2) != 1:
+        raise ShapeError("dq_acc must be fp32 [bh, nq, h] with unit stride along h")
     if dk.stride() != dv.stride() or dk.dtype != dv.dtype or dk.shape != (bh, nk, h):
         raise ShapeError("dk / dv must share shape, strides and dtype")
     a = _lib.TileBwdArgs()
@@ -263,6 +264,7 @@ def tile_backward(q, k, v, dout, lse, delta, *, causal: bool, scale: float,
     a.k_stride_bh, a.k_stride_row = k.stride(0), k.stride(1)
     a.v_stride_bh, a.v_stride_row = v.stride(0), v.stride(1)
     a.do_stride_bh, a.do_stride_row = dout.stride(0), dout.stride(1)
+    a.dq_stride_bh, a.dq_stride_row = dq_acc.stride(0), dq_acc.stride(1)
     a.dkv_stride_bh, a.dkv_stride_row = dk.stride(0), dk.stride(1)
     a.bh, a.nq, a.nk, a.h = bh, nq, nk, h
     a.causal = int(bool(causal))
@@ -280,9 +282,10 @@ def bwd_finalize(dq_acc: torch.Tensor, scale: float, out: torch.Tensor | None = 
     bh, n, h = dq_acc.shape
     if out is None:
         out = torch.empty((bh, n, h), dtype=dtype, device=dq_acc.device)
-    _lib.check(lib.a2d_bwd_finalize(dq_acc.data_ptr(), out.data_ptr(), _dtype_code(out.dtype),
-                                    out.stride(0), out.stride(1), bh, n, h, float(scale),
-                                    _stream(dq_acc)), "a2d_bwd_finalize")
+    _lib.check(lib.a2d_bwd_finalize(dq_acc.data_ptr(), dq_acc.stride(0), dq_acc.stride(1),
+                                    out.data_ptr(), _dtype_code(out.dtype), out.stride(0),
+                                    out.stride(1), bh, n, h, float(scale), _stream(dq_acc)),
+               "a2d_bwd_finalize")
     return out
 
 
