@@ -55,7 +55,7 @@ struct BwdLayout {
   static constexpr int P_BYTES = PS * KSLAB;
   static constexpr int DQ_SLAB = QT * 128;            // QT rows x 32 fp32
   static constexpr int DQ_BYTES = (HD / 32) * DQ_SLAB;
-  static constexpr int ST = 2;                        // Q/dO stages
+  static constexpr int ST = (HD == 128) ? 3 : 2;      // Q/dO stages
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + KV_BYTES;
   static constexpr int OFF_Q = OFF_V + KV_BYTES;
@@ -72,8 +72,9 @@ struct BwdLayout {
   static constexpr int B_DPFULL = B_SFULL + 1;
   static constexpr int B_PREADY = B_DPFULL + 1;
   static constexpr int B_DSREADY = B_PREADY + 1;
-  static constexpr int B_PDSFREE = B_DSREADY + 1;
-  static constexpr int B_DQFULL = B_PDSFREE + 1;
+  static constexpr int B_PFREE = B_DSREADY + 1;
+  static constexpr int B_DSFREE = B_PFREE + 1;
+  static constexpr int B_DQFULL = B_DSFREE + 1;
   static constexpr int B_DQFREE = B_DQFULL + 1;
   static constexpr int B_DONE = B_DQFREE + 1;
   static constexpr int NBAR = B_DONE + 1;
@@ -117,7 +118,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_init(bar(L::B_DPFULL), 1);
     mbar_init(bar(L::B_PREADY), 128);
     mbar_init(bar(L::B_DSREADY), 128);
-    mbar_init(bar(L::B_PDSFREE), 1);
+    mbar_init(bar(L::B_PFREE), 1);
+    mbar_init(bar(L::B_DSFREE), 1);
     mbar_init(bar(L::B_DQFULL), 1);
     mbar_init(bar(L::B_DQFREE), 128);
     mbar_init(bar(L::B_DONE), 1);
@@ -225,10 +227,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         for (int kk = 0; kk < QT / 16; ++kk)
           umma_bf16(tmem + L::TM_DV, kmaj(sb + L::OFF_P, kk, L::KSLAB),
                     make_sdesc(sdo + kk * 2048, L::QSLAB, 1024), idesc_acc, (i > 0 || kk > 0));
+        umma_commit(bar(L::B_PFREE));
         // next S^T as soon as this one has been consumed
         int st1 = st + 1, ph1 = ph;
         if (st1 == L::ST) { st1 = 0; ph1 ^= 1; }
-        if (i + 1 < n_tiles) {
+        const bool more = i + 1 < n_tiles;
+        if (more) {
           mbar_wait(bar(L::B_QFULL + st1), ph1);
           tc_fence_after();
           issue_s(tmem + L::TM_S, sb + L::OFF_K, sb + L::OFF_Q + st1 * L::Q_BYTES);
@@ -241,6 +245,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         for (int kk = 0; kk < QT / 16; ++kk)
           umma_bf16(tmem + L::TM_DK, kmaj(sb + L::OFF_DS, kk, L::KSLAB),
                     make_sdesc(sq + kk * 2048, L::QSLAB, 1024), idesc_acc, (i > 0 || kk > 0));
+        umma_commit(bar(L::B_QEMPTY + st));  // last reader of Q_i / dO_i
+        // next dP^T (its TMEM was consumed when dS_i was produced)
+        if (more) {
+          issue_s(tmem + L::TM_DP, sb + L::OFF_V, sb + L::OFF_DO + st1 * L::Q_BYTES);
+          umma_commit(bar(L::B_DPFULL));
+        }
         // dQ of this sub-tile into TMEM once the drain warps have emptied it
         if (i > 0) {
           mbar_wait(bar(L::B_DQFREE), (i - 1) & 1);
@@ -259,14 +269,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
             umma_bf16(tmem + L::TM_DQ, make_sdesc(sb + L::OFF_DS + kk * 2048, L::KSLAB, 1024),
                       make_sdesc(sb + L::OFF_K + kk * 2048, L::KSLAB, 1024), idesc_dq, kk > 0);
         }
-        umma_commit(bar(L::B_QEMPTY + st));
-        umma_commit(bar(L::B_PDSFREE));
+        umma_commit(bar(L::B_DSFREE));
         umma_commit(bar(L::B_DQFULL));
-        // next dP^T (its TMEM was consumed when dS_i was produced)
-        if (i + 1 < n_tiles) {
-          issue_s(tmem + L::TM_DP, sb + L::OFF_V, sb + L::OFF_DO + st1 * L::Q_BYTES);
-          umma_commit(bar(L::B_DPFULL));
-        }
         st = st1;
         ph = ph1;
       }
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       uint32_t pk[QT / 2];
 #pragma unroll
       for (int c = 0; c < QT; c += 2) pk[c / 2] = pack_bf16(pr[c], pr[c + 1]);
-      if (i > 0) mbar_wait(bar(L::B_PDSFREE), (i - 1) & 1);
+      if (i > 0) mbar_wait(bar(L::B_PFREE), (i - 1) & 1);
       // P^T row jj -> K-major SW128 [128 x QT]
 #pragma unroll
       for (int cc = 0; cc < QT / 8; ++cc) {
@@ -341,6 +345,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           pk[(c0 + c) / 2] = pack_bf16(pr[c0 + c] * (dp[c] - s_del[c0 + c]),
                                        pr[c0 + c + 1] * (dp[c + 1] - s_del[c0 + c + 1]));
       }
+      if (i > 0) mbar_wait(bar(L::B_DSFREE), (i - 1) & 1);
 #pragma unroll
       for (int cc = 0; cc < QT / 8; ++cc) {
         const uint32_t addr = sb + L::OFF_DS + (cc >> 3) * L::KSLAB + jj * 128 +
