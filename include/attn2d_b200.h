@@ -164,6 +164,11 @@ int a2d_lse_merge(const float* o_parts, const float* lse_parts, int32_t k_parts,
 int a2d_selftest_umma(const void* a, const void* b, float* d, int32_t n,
                       int32_t b_mn_major, void* stream);
 
+/* Diagnostic: tcgen05 issue-rate probe; cycles_out[ctas] receives the cycles
+ * one CTA spent issuing `iters` K=128 units of MMA shape `variant`. */
+int a2d_bench_umma(int32_t variant, int32_t iters, int64_t* cycles_out, int32_t ctas,
+                   void* stream);
+
 int a2d_abi_version(void);
 const char* a2d_last_error(void);
 int a2d_num_sms(void);

@@ -14,7 +14,8 @@ from pathlib import Path
 
 from .errors import ShapeError, UnsupportedError
 
-LIB_PATH = Path(__file__).resolve().parent / "libattn2d_b200.so"
+LIB_PATH = Path(os.environ.get("A2D_LIB_PATH") or
+                Path(__file__).resolve().parent / "libattn2d_b200.so")
 ABI_VERSION = 1
 MAX_BLOCKS = 16
 
@@ -24,7 +25,7 @@ F32, BF16 = 0, 1
 
 # every symbol include/attn2d_b200.h declares
 EXPORTS = ("a2d_tile_fwd", "a2d_bwd_preprocess", "a2d_tile_bwd", "a2d_bwd_finalize",
-           "a2d_lse_merge", "a2d_selftest_umma", "a2d_abi_version", "a2d_last_error",
+           "a2d_lse_merge", "a2d_selftest_umma", "a2d_bench_umma", "a2d_abi_version", "a2d_last_error",
            "a2d_num_sms")
 
 
@@ -84,6 +85,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     lib.a2d_lse_merge.argtypes = [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int64,
                                   c_int32, c_int64, c_void_p, c_int32, c_int64, c_void_p,
                                   c_void_p]
+    lib.a2d_bench_umma.argtypes = [c_int32, c_int32, c_void_p, c_int32, c_void_p]
     lib.a2d_selftest_umma.argtypes = [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p]
     lib.a2d_last_error.restype = ctypes.c_char_p
     for name in EXPORTS:

@@ -229,6 +229,11 @@ int a2d_lse_merge(const float* o_parts, const float* lse_parts, int32_t k_parts,
                           static_cast<cudaStream_t>(stream));
 }
 
+int a2d_bench_umma(int32_t variant, int32_t iters, int64_t* cycles_out, int32_t ctas, void* stream) {
+  return launch_bench_umma(variant, iters, reinterpret_cast<long long*>(cycles_out), ctas,
+                           static_cast<cudaStream_t>(stream));
+}
+
 int a2d_selftest_umma(const void* a, const void* b, float* d, int32_t n, int32_t b_mn_major,
                       void* stream) {
   if (n != 64 && n != 128) return set_error(A2D_EUNSUPPORTED, "n must be 64 or 128");

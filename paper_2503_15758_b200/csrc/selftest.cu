@@ -96,4 +96,78 @@ int launch_selftest_umma(const void* a, const void* b, float* d, int n, int b_mn
   return check_launch("selftest_kernel");
 }
 
+namespace {
+
+// tcgen05 issue-rate probe: one elected thread per CTA issues `iters` units
+// of K=128 (8 x K16 MMAs) of one operand shape / majorness, back to back.
+__global__ void __launch_bounds__(128, 1) umma_bench_kernel(int variant, int iters,
+                                                            long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sa = smem_u32(smem);
+  const uint32_t sbb = sa + 65536;
+  const uint32_t sbar = sbb + 65536;
+  const uint32_t stm = sbar + 8;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(sbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    tmem_alloc(stm, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + (stm - sa));
+  if (threadIdx.x == 0) {
+    int N = 128, am = 0, bm = 0;
+    switch (variant) {
+      case 0: N = 128; break;
+      case 1: N = 128; bm = 1; break;
+      case 2: N = 64; break;
+      case 3: N = 64; am = 1; bm = 1; break;
+      case 4: N = 256; break;
+      case 5: N = 128; am = 1; bm = 1; break;
+      case 6: N = 64; bm = 1; break;
+      default: N = 32; break;
+    }
+    const uint32_t idesc = make_idesc_bf16(128, N, am, bm);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint64_t ad = am ? make_sdesc(sa + kk * 2048, SLAB, 1024)
+                               : make_sdesc(sa + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = bm ? make_sdesc(sbb + kk * 2048, SLAB, 1024)
+                               : make_sdesc(sbb + (kk >> 2) * (N * 128) + (kk & 3) * 32, 16, 1024);
+        umma_bf16(tmem + (it & 1) * 256, ad, bd, idesc, kk > 0);
+      }
+    }
+    umma_commit(sbar);
+    mbar_wait(sbar, 0);
+    const long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+int launch_bench_umma(int variant, int iters, long long* out, int ctas, cudaStream_t stream) {
+  const int smem = 2 * 65536 + 64 + 1024;
+  cudaError_t e =
+      cudaFuncSetAttribute(umma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(bench)");
+  umma_bench_kernel<<<ctas, 128, smem, stream>>>(variant, iters, out);
+  return check_launch("umma_bench_kernel");
+}
+
 }  // namespace a2d

@@ -170,6 +170,64 @@ A2D_DEV float lg2(float x) {
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+A2D_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// packed fp32x2 (FFMA2 / FADD2 on sm_100)
+A2D_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+A2D_DEV float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// 2^x for finite x <= ~8 on the FMA/ALU pipes (MUFU offload): round-to-nearest
+// split x = n + f, f in [-0.5, 0.5], near-minimax cubic for 2^f (max rel err
+// 1.0e-4, far below the bf16 rounding of P), 2^n folded into the exponent.
+// Inputs below -126 flush towards 2^-126; -inf is NOT supported (masked
+// tiles use the MUFU path).
+A2D_DEV float2 exp2_poly2(float2 x) {
+  const float2 lo = make_float2(-126.f, -126.f);
+  x = make_float2(fmaxf(x.x, lo.x), fmaxf(x.y, lo.y));
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = fadd2(x, magic);
+  const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fadd2(x, make_float2(-r.x, -r.y));
+  float2 p = ffma2(f, make_float2(0.05500893f, 0.05500893f), make_float2(0.24221098f, 0.24221098f));
+  p = ffma2(p, f, make_float2(0.69328293f, 0.69328293f));
+  p = ffma2(p, f, make_float2(1.0f, 1.0f));
+  const int ex = (__float_as_int(t.x) << 23) + __float_as_int(p.x);
+  const int ey = (__float_as_int(t.y) << 23) + __float_as_int(p.y);
+  return make_float2(__int_as_float(ex), __int_as_float(ey));
+}
+// max over 128 values: 8 independent FMNMX3 chains, then a 3-level tree
+A2D_DEV float rowmax128(const float* s) {
+  float m[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = fmaxf(s[i], s[8 + i]);
+#pragma unroll
+  for (int k = 16; k < 128; k += 16) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = fmax3(m[i], s[k + i], s[k + 8 + i]);
+  }
+  const float a = fmax3(m[0], m[1], m[2]);
+  const float b = fmax3(m[3], m[4], m[5]);
+  const float c = fmaxf(m[6], m[7]);
+  return fmax3(a, b, c);
+}
 A2D_DEV uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

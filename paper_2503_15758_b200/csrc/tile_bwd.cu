@@ -24,6 +24,14 @@
 #include "tiles.cuh"
 #include "kernels.h"
 
+#ifdef A2D_X_MMA_ONLY
+#define XWAIT(b, ph) ((void)0)
+#define XLOOP 0
+#else
+#define XWAIT(b, ph) mbar_wait(b, ph)
+#define XLOOP 1
+#endif
+
 namespace a2d {
 namespace {
 
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const uint32_t sq = sb + L::OFF_Q + st * L::Q_BYTES;
         const uint32_t sdo = sb + L::OFF_DO + st * L::Q_BYTES;
         // dV += P^T dO_i : A = P^T [128 x QT] K-major, B = dO_i [QT x HD] MN-major
-        mbar_wait(bar(L::B_PREADY), i & 1);
+        XWAIT(bar(L::B_PREADY), i & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < QT / 16; ++kk)
@@ -239,7 +247,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           umma_commit(bar(L::B_SFULL));
         }
         // dK += dS^T Q_i : A = dS^T K-major, B = Q_i MN-major
-        mbar_wait(bar(L::B_DSREADY), i & 1);
+        XWAIT(bar(L::B_DSREADY), i & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < QT / 16; ++kk)
@@ -253,7 +261,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         // dQ of this sub-tile into TMEM once the drain warps have emptied it
         if (i > 0) {
-          mbar_wait(bar(L::B_DQFREE), (i - 1) & 1);
+          XWAIT(bar(L::B_DQFREE), (i - 1) & 1);
           tc_fence_after();
         }
         if constexpr (L::DQ_T) {
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     TileCursor cur;
     cur.start(qr);
     int st = 0, sph = 0;
-    for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
+    for (int i = 0; i < (XLOOP ? n_tiles : 0); ++i, cur.next(qr)) {
       const TileRef qt = tile_ref(p.q_map, p.nq, cur.row0(p.q_map, QT), QT);
       mbar_wait(bar(L::B_QFULL + st), sph);  // orders the producer's lse/delta stores
       int first = 0;  // first visible query column of this key row
@@ -315,7 +323,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tmem_wait_ld();
 #pragma unroll
       for (int c = 0; c < QT; ++c) {
+#ifndef A2D_X_NO_EXP
         const float e = ex2(fmaf(pr[c], sl2, -s_lse[c]));
+#else
+        const float e = fmaf(pr[c], sl2, -s_lse[c]);
+#endif
         pr[c] = (c >= first) ? e : 0.f;
       }
       uint32_t pk[QT / 2];
@@ -407,7 +419,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
     TileCursor cur;
     cur.start(qr);
-    for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
+    for (int i = 0; i < (XLOOP ? n_tiles : 0); ++i, cur.next(qr)) {
       const int qrow = cur.row0(p.q_map, QT);
       mbar_wait(bar(L::B_DQFULL), i & 1);
       tc_fence_after();
@@ -445,7 +457,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
+#ifndef A2D_X_NO_DQ_REDUCE
       if (t == 0) {
+#else
+      if (false) {
+#endif
 #pragma unroll
         for (int s = 0; s < HD / 32; ++s)
           tma_reduce_add_3d(&tm_dq, sb + L::OFF_DQ + s * L::DQ_SLAB, s * 32, qrow, bh);

@@ -24,6 +24,19 @@
 #include "tiles.cuh"
 #include "kernels.h"
 
+#ifdef A2D_X_MMA_ONLY
+#define XWAIT(b, ph) ((void)0)
+#define XLOOP 0
+#else
+#define XWAIT(b, ph) mbar_wait(b, ph)
+#define XLOOP 1
+#endif
+#ifdef A2D_X_NO_EXP
+#define XEX2(x) (x)
+#else
+#define XEX2(x) ex2(x)
+#endif
+
 namespace a2d {
 
 namespace {
@@ -168,7 +181,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       issue_qk(0);
       for (int j = 0; j < n_tiles; ++j) {
         if (j + 1 < n_tiles) issue_qk(j + 1);
-        mbar_wait(bar(L::B_PFULL), j & 1);
+        XWAIT(bar(L::B_PFULL), j & 1);
         mbar_wait(bar(L::B_VFULL + vs), vph);
         tc_fence_after();
         const uint32_t vbase = sb + L::OFF_V + vs * L::TILE_BYTES;
@@ -193,7 +206,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     float l_run = 0.f;
     TileCursor cur;
     cur.start(kr);
-    for (int j = 0; j < n_tiles; ++j, cur.next(kr)) {
+    for (int j = 0; j < (XLOOP ? n_tiles : 0); ++j, cur.next(kr)) {
       const TileRef kt = tile_ref(p.k_map, p.nk, cur.row0(p.k_map));
       const PairMask pm = pair_mask(p.q_map, qt, kt, causal);
       int lim = TILE - 1;
@@ -211,9 +224,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         for (int jj = 0; jj < TILE; ++jj)
           if (jj > lim) s[jj] = -INFINITY;
       }
-      float mx = s[0];
-#pragma unroll
-      for (int jj = 1; jj < TILE; ++jj) mx = fmaxf(mx, s[jj]);
+      const float mx = rowmax128(s);
       const float m_new = fmaxf(m_run, mx * sl2);
       float alpha = 1.f;
       if (m_new > m_run + kRescaleThreshold) {
@@ -222,16 +233,30 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       }
       const float mb = (m_run == -INFINITY) ? 0.f : m_run;
       uint32_t pk[TILE / 2];
-      float sum0 = 0.f, sum1 = 0.f;
+      float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+      const float2 sc = make_float2(sl2, sl2), nb = make_float2(-mb, -mb);
+      if (pm.partial) {  // masked entries are -inf: the exact MUFU path keeps them 0
 #pragma unroll
-      for (int jj = 0; jj < TILE; jj += 2) {
-        const float p0 = ex2(fmaf(s[jj], sl2, -mb));
-        const float p1 = ex2(fmaf(s[jj + 1], sl2, -mb));
-        sum0 += p0;
-        sum1 += p1;
-        pk[jj / 2] = pack_bf16(p0, p1);
+        for (int jj = 0; jj < TILE; jj += 2) {
+          const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
+          const float2 e = make_float2(XEX2(x.x), XEX2(x.y));
+          acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
+          pk[jj / 2] = pack_bf16(e.x, e.y);
+        }
+      } else {  // a quarter of the exponentials on the FMA pipe (MUFU offload)
+#pragma unroll
+        for (int jj = 0; jj < TILE; jj += 2) {
+          const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
+          float2 e;
+          if (((jj >> 1) & 3) == 3) e = exp2_poly2(x);
+          else e = make_float2(XEX2(x.x), XEX2(x.y));
+          acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
+          pk[jj / 2] = pack_bf16(e.x, e.y);
+        }
       }
-      l_run = l_run * alpha + (sum0 + sum1);
+      const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+      const float2 a = fadd2(a01, a23);
+      l_run = l_run * alpha + (a.x + a.y);
 
       // P buffer and O are free once PV_{j-1} has completed.
       if (j > 0) {
