@@ -28,6 +28,8 @@ int launch_bwd_finalize(const float* dq_acc, long long asbh, long long asrow, vo
 int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, long long s_row,
                     long long s_bh, int box_rows);
 int bwd_q_tile_rows(int h);
+int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                  const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream);
 int launch_bench_umma(int variant, int iters, long long* out, int ctas, cudaStream_t stream);
 int launch_selftest_umma(const void* a, const void* b, float* d, int n, int b_mn_major,
                          cudaStream_t stream);

@@ -46,21 +46,46 @@ __global__ void __launch_bounds__(128, 1)
   }
   fence_proxy_async_smem();
   if (warp == 0) {
-    tmem_alloc(stm, 128);
+    tmem_alloc(stm, 256);
     tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + (stm - sa));
+  const bool a_tmem = (b_mn & 2) != 0;
+  b_mn &= 1;
+  if (a_tmem) {
+    // A row `row` -> TMEM lane `row`, columns [128, 192): bf16 pairs (2c, 2c+1) in column c
+    const int row = warp * 32 + (threadIdx.x & 31);
+    for (int c0 = 0; c0 < 64; c0 += 32) {
+      float pk[32];
+      for (int i = 0; i < 32; ++i) {
+        const __nv_bfloat16 lo = a[row * 128 + 2 * (c0 + i)];
+        const __nv_bfloat16 hi = a[row * 128 + 2 * (c0 + i) + 1];
+        const uint32_t u = (uint32_t)__bfloat16_as_ushort(lo) |
+                           ((uint32_t)__bfloat16_as_ushort(hi) << 16);
+        pk[i] = __uint_as_float(u);
+      }
+      tmem_st32(tmem + (uint32_t(warp * 32) << 16) + 128 + c0, pk);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   if (threadIdx.x == 0) {
     const uint32_t idesc = make_idesc_bf16(128, n, 0, b_mn);
     for (int kk = 0; kk < 8; ++kk) {
-      const uint64_t ad = make_sdesc(sa + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
       uint64_t bd;
       if (b_mn) bd = make_sdesc(sbb + kk * 2048, SLAB, 1024);
       else bd = make_sdesc(sbb + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
-      umma_bf16(tmem, ad, bd, idesc, kk > 0);
+      if (a_tmem) {
+        umma_bf16_ts(tmem, tmem + 128 + kk * 8, bd, idesc, kk > 0);
+      } else {
+        const uint64_t ad = make_sdesc(sa + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
+        umma_bf16(tmem, ad, bd, idesc, kk > 0);
+      }
     }
     umma_commit(sbar);
   }
@@ -78,7 +103,7 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc(tmem, 128);
+    tmem_dealloc(tmem, 256);
   }
 }
 
@@ -132,18 +157,34 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int variant, int ite
       case 4: N = 256; break;
       case 5: N = 128; am = 1; bm = 1; break;
       case 6: N = 64; bm = 1; break;
+      case 7: N = 128; break;            // A from TMEM (TS)
+      case 8: N = 128; bm = 1; break;    // TS, B MN-major
+      case 9: N = 64; break;             // TS
+      case 10: N = 256; break;           // TS
       default: N = 32; break;
     }
+    const bool ts = variant >= 7 && variant <= 10;
     const uint32_t idesc = make_idesc_bf16(128, N, am, bm);
-    const long long t0 = clock64();
-    for (int it = 0; it < iters; ++it) {
+    uint64_t ad[8], bd[8];
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const uint64_t ad = am ? make_sdesc(sa + kk * 2048, SLAB, 1024)
-                               : make_sdesc(sa + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
-        const uint64_t bd = bm ? make_sdesc(sbb + kk * 2048, SLAB, 1024)
-                               : make_sdesc(sbb + (kk >> 2) * (N * 128) + (kk & 3) * 32, 16, 1024);
-        umma_bf16(tmem + (it & 1) * 256, ad, bd, idesc, kk > 0);
+    for (int kk = 0; kk < 8; ++kk) {
+      ad[kk] = am ? make_sdesc(sa + kk * 2048, SLAB, 1024)
+                  : make_sdesc(sa + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
+      bd[kk] = bm ? make_sdesc(sbb + kk * 2048, SLAB, 1024)
+                  : make_sdesc(sbb + (kk >> 2) * (N * 128) + (kk & 3) * 32, 16, 1024);
+    }
+    const long long t0 = clock64();
+    if (ts) {
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16_ts(tmem + (it & 1) * 128, tmem + 384 + kk * 8, bd[kk], idesc, kk > 0);
+      }
+    } else {
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16(tmem + (it & 1) * 256, ad[kk], bd[kk], idesc, kk > 0);
       }
     }
     umma_commit(sbar);

@@ -505,12 +505,28 @@ int launch_bwd_hd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUten
   return check_launch("bwd_kernel");
 }
 
+// H = 128 runs the N=128-shaped kernel (tile_bwd128.cu); A2D_BWD_V1=1 selects
+// this file's 64-query design instead (kept for A/B measurement).
+static bool use_v1_for_128() {
+  static const bool v1 = [] {
+    const char* e = getenv("A2D_BWD_V1");
+    return e != nullptr && e[0] == '1';
+  }();
+  return v1;
+}
+
 int launch_tile_bwd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream) {
-  if (a.h == 128) return launch_bwd_hd<128>(a, tq, tk, tv, tdo, stream);
+  if (a.h == 128) {
+    if (!use_v1_for_128()) return launch_bwd128(a, tq, tk, tv, tdo, stream);
+    return launch_bwd_hd<128>(a, tq, tk, tv, tdo, stream);
+  }
   return launch_bwd_hd<64>(a, tq, tk, tv, tdo, stream);
 }
 
-int bwd_q_tile_rows(int h) { return h == 128 ? BwdLayout<128>::QT : BwdLayout<64>::QT; }
+int bwd_q_tile_rows(int h) {
+  if (h == 128) return use_v1_for_128() ? BwdLayout<128>::QT : TILE;
+  return BwdLayout<64>::QT;
+}
 
 }  // namespace a2d

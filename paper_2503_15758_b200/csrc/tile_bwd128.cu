@@ -1,0 +1,435 @@
+// tile_bwd128.cu — Attention2D tile backward for head dim 128 on sm_100a.
+//
+// Same recurrence as tile_bwd.cu (the reference's flash_backward,
+// numpy_backend.py:46-62) but shaped so that EVERY tcgen05.mma has N = 128,
+// the shape that runs at the full 8192 flop/clk/SM (tools/umma_rate.py: the
+// N = 64 shapes of the 64-query design are shared-memory bound at 61-70%).
+//
+// One CTA = one 128-key tile of one head; it sweeps 128-query tiles:
+//   S^T  = K Q_i^T            -> TMEM X      (SS, M128 N128)
+//   P^T  = exp2(S^T c - lse)  -> TMEM X (bf16, in place)          [P/dS warpgroups]
+//   dV  += P^T dO_i           (TS: A from TMEM)                   -> TMEM dV
+//   dP^T = V dO_i^T           -> TMEM X (after dV in pipe order)
+//   dS^T = P^T (dP^T - delta) -> smem (bf16, 128B swizzle)          [P/dS warpgroups]
+//   dK  += dS^T Q_i           (SS)                                 -> TMEM dK
+//   dQ^T = K^T dS^T           (SS, both MN-major)                  -> TMEM dQ
+//   dQ   -> 2 x 16 KB fp32 staging -> TMA bulk reduce-add into dq_acc
+// S_{i+1} is issued as soon as dS_i is out of TMEM, so the exponentials of
+// tile i+1 overlap dK_i and dQ_i on the tensor pipe.
+//
+// TMEM (512 cols): dV [0,128) dK [128,256) X [256,384) dQ^T [384,512).
+// SMEM (231.6 KB): K, V, 2 x Q, dO, dS^T, 2 x dQ staging, LSE/delta stats.
+// Warps (448 threads): 0 TMA producer, 1 MMA issuer, 2-5 P/dS warpgroup A
+// (query columns 0-63), 6-9 warpgroup B (64-127), 10-13 dQ drain.
+#include "sm100.cuh"
+#include "tiles.cuh"
+#include "kernels.h"
+
+namespace a2d {
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int THREADS = 448;
+constexpr int SLAB = 128 * 128;  // 128 rows x 128 B
+constexpr int TILE_B = 2 * SLAB; // one 128 x 128 bf16 tile
+constexpr int OFF_K = 0;
+constexpr int OFF_V = OFF_K + TILE_B;
+constexpr int OFF_Q = OFF_V + TILE_B;      // 2 stages
+constexpr int OFF_DO = OFF_Q + 2 * TILE_B;
+constexpr int OFF_DS = OFF_DO + TILE_B;
+constexpr int STG = 4 * 32 * 128;          // one staging buffer: 4 slabs of [32 q][32 h] fp32
+constexpr int OFF_DQ = OFF_DS + TILE_B;    // 2 buffers
+constexpr int OFF_STAT = OFF_DQ + 2 * STG; // [2][2][128] fp32
+constexpr int OFF_BAR = OFF_STAT + 2 * 2 * 128 * 4;
+enum {
+  B_KV, B_QFULL0, B_QFULL1, B_QEMPTY0, B_QEMPTY1, B_DOFULL, B_DOEMPTY, B_SFULL, B_PREADY,
+  B_DPFULL, B_DSREADY, B_DSFREE, B_DQFULL, B_DQFREE, B_DONE, NBAR
+};
+constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
+constexpr int SMEM = OFF_TMEMPTR + 16;
+static_assert(SMEM <= 232448, "shared memory budget");
+constexpr uint32_t TM_DV = 0, TM_DK = 128, TM_X = 256, TM_DQ = 384;
+
+__global__ void __launch_bounds__(THREADS, 1)
+    bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                  const __grid_constant__ CUtensorMap tm_dq,
+                  const __grid_constant__ a2d_tile_bwd_args p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sb = smem_u32(smem);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int bh = blockIdx.y;
+  const int kt_idx = blockIdx.x;
+  auto bar = [&](int i) { return sb + OFF_BAR + 8 * i; };
+  float* stat = reinterpret_cast<float*>(smem + OFF_STAT);
+  if ((sb & 1023) != 0) __trap();
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(B_KV), 1);
+    mbar_init(bar(B_QFULL0), 1);
+    mbar_init(bar(B_QFULL1), 1);
+    mbar_init(bar(B_QEMPTY0), 1);
+    mbar_init(bar(B_QEMPTY1), 1);
+    mbar_init(bar(B_DOFULL), 1);
+    mbar_init(bar(B_DOEMPTY), 1);
+    mbar_init(bar(B_SFULL), 1);
+    mbar_init(bar(B_PREADY), 256);
+    mbar_init(bar(B_DPFULL), 1);
+    mbar_init(bar(B_DSREADY), 256);
+    mbar_init(bar(B_DSFREE), 1);
+    mbar_init(bar(B_DQFULL), 1);
+    mbar_init(bar(B_DQFREE), 128);
+    mbar_init(bar(B_DONE), 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_dq);
+  }
+  if (warp == 1) {
+    tmem_alloc(sb + OFF_TMEMPTR, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + OFF_TMEMPTR);
+
+  const bool causal = p.causal != 0;
+  const TileRef kt = tile_ref(p.k_map, p.nk, kt_idx * TILE);
+  TileRange qr;
+  query_range(p.q_map, p.nq, causal, kt.gmin, qr, TILE);
+  const int n_tiles = qr.total;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (n_tiles > 0) {
+      if (lane == 0) {
+        mbar_expect_tx(bar(B_KV), 2 * TILE_B);
+        for (int s = 0; s < 2; ++s) {
+          tma_load_3d(sb + OFF_K + s * SLAB, &tm_k, bar(B_KV), s * 64, kt.row0, bh);
+          tma_load_3d(sb + OFF_V + s * SLAB, &tm_v, bar(B_KV), s * 64, kt.row0, bh);
+        }
+      }
+      TileCursor cur;
+      cur.start(qr);
+      for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
+        const int qrow = cur.row0(p.q_map);
+        const int qs = i & 1;
+        mbar_wait(bar(B_QEMPTY0 + qs), ((i >> 1) & 1) ^ 1);
+        float* s_lse = stat + qs * 256;
+        float* s_del = s_lse + 128;
+        for (int r = lane; r < 128; r += 32) {
+          const int gr = qrow + r;
+          float l2 = INFINITY, dl = 0.f;
+          if (gr < p.nq) {
+            const float l = p.lse[(long long)bh * p.nq + gr];
+            l2 = (l == -INFINITY) ? INFINITY : l * kLog2e;
+            dl = p.delta[(long long)bh * p.nq + gr];
+          }
+          s_lse[r] = l2;
+          s_del[r] = dl;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_expect_tx(bar(B_QFULL0 + qs), TILE_B);
+          for (int s = 0; s < 2; ++s)
+            tma_load_3d(sb + OFF_Q + qs * TILE_B + s * SLAB, &tm_q, bar(B_QFULL0 + qs), s * 64,
+                        qrow, bh);
+          mbar_wait(bar(B_DOEMPTY), (i & 1) ^ 1);
+          mbar_expect_tx(bar(B_DOFULL), TILE_B);
+          for (int s = 0; s < 2; ++s)
+            tma_load_3d(sb + OFF_DO + s * SLAB, &tm_do, bar(B_DOFULL), s * 64, qrow, bh);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && n_tiles > 0) {
+      constexpr uint32_t id_ss = make_idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
+      constexpr uint32_t id_kmn = make_idesc_bf16(128, 128, 0, 1);  // P^T dO, dS^T Q
+      constexpr uint32_t id_mnmn = make_idesc_bf16(128, 128, 1, 1); // K^T dS^T
+      auto kmaj = [](uint32_t base, int kk) {
+        return make_sdesc(base + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
+      };
+      auto mnmaj = [](uint32_t base, int kk) { return make_sdesc(base + kk * 2048, SLAB, 1024); };
+      auto issue_s = [&](uint32_t a_base, uint32_t b_base) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16(tmem + TM_X, kmaj(a_base, kk), kmaj(b_base, kk), id_ss, kk > 0);
+      };
+      mbar_wait(bar(B_KV), 0);
+      mbar_wait(bar(B_QFULL0), 0);
+      tc_fence_after();
+      issue_s(sb + OFF_K, sb + OFF_Q);
+      umma_commit(bar(B_SFULL));
+      for (int i = 0; i < n_tiles; ++i) {
+        const int qs = i & 1;
+        const uint32_t sq = sb + OFF_Q + qs * TILE_B;
+        // dV += P^T dO_i (P^T in TMEM: warpgroup A's 64 queries at X+0, B's at X+64)
+        mbar_wait(bar(B_DOFULL), i & 1);
+        mbar_wait(bar(B_PREADY), i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16_ts(tmem + TM_DV, tmem + TM_X + (kk >> 2) * 64 + (kk & 3) * 8,
+                       mnmaj(sb + OFF_DO, kk), id_kmn, (i > 0 || kk > 0));
+        // dP^T = V dO_i^T overwrites X after dV has read P^T (in-order pipe)
+        issue_s(sb + OFF_V, sb + OFF_DO);
+        umma_commit(bar(B_DOEMPTY));
+        umma_commit(bar(B_DPFULL));
+        // once dS_i is out of TMEM, X takes S_{i+1}
+        mbar_wait(bar(B_DSREADY), i & 1);
+        tc_fence_after();
+        if (i + 1 < n_tiles) {
+          mbar_wait(bar(B_QFULL0 + (qs ^ 1)), ((i + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_s(sb + OFF_K, sb + OFF_Q + (qs ^ 1) * TILE_B);
+          umma_commit(bar(B_SFULL));
+        }
+        // dK += dS^T Q_i
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16(tmem + TM_DK, kmaj(sb + OFF_DS, kk), mnmaj(sq, kk), id_kmn, (i > 0 || kk > 0));
+        umma_commit(bar(B_QEMPTY0 + qs));
+        // dQ^T = K^T dS^T once the drain warps have emptied dQ
+        if (i > 0) {
+          mbar_wait(bar(B_DQFREE), (i - 1) & 1);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16(tmem + TM_DQ, mnmaj(sb + OFF_K, kk), mnmaj(sb + OFF_DS, kk), id_mnmn, kk > 0);
+        umma_commit(bar(B_DSFREE));
+        umma_commit(bar(B_DQFULL));
+      }
+      umma_commit(bar(B_DONE));
+    }
+  } else if (warp < 10) {
+    // ------------------------------------------------------------ P / dS warpgroups
+    const int wg = (warp - 2) >> 2;  // 0: query columns 0-63, 1: 64-127
+    const int quarter = warp & 3;
+    const int jj = quarter * 32 + lane;  // key row within the tile
+    const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+    const int c0 = wg * 64;
+    const float sl2 = p.scale * kLog2e;
+    const bool row_ok = jj < kt.nvalid;
+    TileCursor cur;
+    cur.start(qr);
+    for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
+      const int qs = i & 1;
+      const TileRef qt = tile_ref(p.q_map, p.nq, cur.row0(p.q_map), TILE);
+      int first = 0;  // first visible query column of this key row
+      bool full = true;
+      if (causal) {
+        if (p.q_map.mode == A2D_IDX_ARRAY) {
+          PairMask pm;
+          pm.partial = true;
+          pm.thr = 0;
+          pm.kvalid = kt.nvalid;
+          first = col_first(p.q_map, p.k_map, qt, kt, pm, true, jj);
+          full = false;
+        } else {
+          long long thr = ceil_div_s(kt.gmin - qt.gmin, p.q_map.stride);
+          thr = max(-(long long)(2 * TILE), min((long long)(2 * TILE), thr));
+          first = jj + (int)thr;
+          full = thr <= -(TILE - 1);
+        }
+      }
+      if (!row_ok) first = TILE;
+      full = full && kt.nvalid == TILE && qt.nvalid == TILE;
+      const float* s_lse = stat + qs * 256 + c0;
+      const float* s_del = s_lse + 128;
+      mbar_wait(bar(B_QFULL0 + qs), (i >> 1) & 1);  // orders the producer's stats stores
+      mbar_wait(bar(B_SFULL), i & 1);
+      tc_fence_after();
+      float pr[64];
+      tmem_ld32(tmem + lane_addr + TM_X + c0, pr);
+      tmem_ld32(tmem + lane_addr + TM_X + c0 + 32, pr + 32);
+      tmem_wait_ld();
+      uint32_t pk[32];
+      const float2 sc = make_float2(sl2, sl2);
+      if (full) {
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          const float2 x = ffma2(make_float2(pr[c], pr[c + 1]), sc,
+                                 make_float2(-s_lse[c], -s_lse[c + 1]));
+          const float2 e = (((c >> 1) & 3) == 3) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          pr[c] = e.x;
+          pr[c + 1] = e.y;
+          pk[c >> 1] = pack_bf16(e.x, e.y);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          const float2 x = ffma2(make_float2(pr[c], pr[c + 1]), sc,
+                                 make_float2(-s_lse[c], -s_lse[c + 1]));
+          const float e0 = (c0 + c >= first) ? ex2(x.x) : 0.f;
+          const float e1 = (c0 + c + 1 >= first) ? ex2(x.y) : 0.f;
+          pr[c] = e0;
+          pr[c + 1] = e1;
+          pk[c >> 1] = pack_bf16(e0, e1);
+        }
+      }
+      // P^T (bf16 pairs) over the first 32 columns of this warpgroup's S slice
+      tmem_st32(tmem + lane_addr + TM_X + c0, reinterpret_cast<const float*>(pk));
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar(B_PREADY));
+
+      mbar_wait(bar(B_DPFULL), i & 1);
+      tc_fence_after();
+      // dS = P (dP - delta), with P re-read from its bf16 pairs (the same
+      // rounded P that fed dV; keeps the warpgroup within 128 registers)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float dp[32];
+        tmem_ld32(tmem + lane_addr + TM_X + c0 + 32 * h, dp);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const float2 d = fadd2(make_float2(dp[c], dp[c + 1]),
+                                 make_float2(-s_del[32 * h + c], -s_del[32 * h + c + 1]));
+          const uint32_t pp = pk[(32 * h + c) >> 1];
+          const float2 pf = make_float2(__uint_as_float(pp << 16), __uint_as_float(pp & 0xffff0000u));
+          pk[(32 * h + c) >> 1] = pack_bf16(pf.x * d.x, pf.y * d.y);
+        }
+      }
+      tc_fence_before();  // the dP^T loads are done before X is handed back
+      if (i > 0) mbar_wait(bar(B_DSFREE), (i - 1) & 1);
+      // dS^T row jj -> K-major SW128 slab `wg` (64 queries = 128 B per row)
+      const uint32_t drow = sb + OFF_DS + wg * SLAB + jj * 128;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc)
+        st_shared_v4(drow + ((cc ^ (jj & 7)) << 4), pk[cc * 4], pk[cc * 4 + 1], pk[cc * 4 + 2],
+                     pk[cc * 4 + 3]);
+      fence_proxy_async_smem();
+      mbar_arrive(bar(B_DSREADY));
+    }
+    // ------------------------------------------------------------ dV (A) / dK (B) epilogue
+    if (n_tiles > 0) {
+      mbar_wait(bar(B_DONE), 0);
+      tc_fence_after();
+    }
+    const uint32_t col0 = wg == 0 ? TM_DV : TM_DK;
+    void* base = wg == 0 ? p.dv : p.dk;
+    const float mul = wg == 0 ? 1.f : p.scale;
+    const long long grow = (long long)kt.row0 + jj;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float v[32];
+      if (n_tiles > 0) {
+        tmem_ld32(tmem + lane_addr + col0 + c * 32, v);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0.f;
+      }
+      if (!row_ok) continue;
+      const long long off = (long long)bh * p.dkv_stride_bh + grow * p.dkv_stride_row + c * 32;
+      if (p.dkv_dtype == A2D_F32) {
+        float* dst = reinterpret_cast<float*>(base) + off;
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          *reinterpret_cast<float4*>(dst + e) =
+              make_float4(v[e] * mul, v[e + 1] * mul, v[e + 2] * mul, v[e + 3] * mul);
+      } else {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(base) + off;
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          uint4 u;
+          u.x = pack_bf16(v[e] * mul, v[e + 1] * mul);
+          u.y = pack_bf16(v[e + 2] * mul, v[e + 3] * mul);
+          u.z = pack_bf16(v[e + 4] * mul, v[e + 5] * mul);
+          u.w = pack_bf16(v[e + 6] * mul, v[e + 7] * mul);
+          *reinterpret_cast<uint4*>(dst + e) = u;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ dQ drain
+    const int quarter = warp & 3;
+    const int h = quarter * 32 + lane;  // TMEM lane = head dim of dQ^T
+    const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+    const int hc = (h & 31) >> 2, he = (h & 3) * 4;
+    int round = 0;
+    TileCursor cur;
+    cur.start(qr);
+    for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
+      const int qrow = cur.row0(p.q_map);
+      mbar_wait(bar(B_DQFULL), i & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float v[64];
+        tmem_ld32(tmem + lane_addr + TM_DQ + 64 * half, v);
+        tmem_ld32(tmem + lane_addr + TM_DQ + 64 * half + 32, v + 32);
+        tmem_wait_ld();
+        if (half == 1) {
+          tc_fence_before();
+          mbar_arrive(bar(B_DQFREE));
+        }
+#pragma unroll
+        for (int r2 = 0; r2 < 2; ++r2, ++round) {
+          const uint32_t buf = sb + OFF_DQ + (round & 1) * STG;
+          if (h == 0) bulk_wait_group_read<1>();  // this buffer's previous reduce has read it
+          named_bar_sync(1, 128);
+          const uint32_t slab = buf + (h >> 5) * (32 * 128);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const uint32_t addr = slab + q * 128 + ((hc ^ (q & 7)) << 4) + he;
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v[32 * r2 + q]) : "memory");
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (h == 0) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+              tma_reduce_add_3d_g(&tm_dq, buf + s * (32 * 128), s * 32,
+                                  qrow + 64 * half + 32 * r2, bh);
+            bulk_commit_group();
+          }
+        }
+      }
+    }
+    if (h == 0) bulk_wait_group_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                  const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream) {
+  static bool configured[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!configured[dev & 63]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(bwd128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(bwd128)");
+    configured[dev & 63] = true;
+  }
+  CUtensorMap tdq;
+  int rc = make_map_f32_dq(&tdq, a.dq_acc, 128, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh, 32);
+  if (rc) return rc;
+  const int k_tiles = (a.k_map.mode == A2D_IDX_AFFINE && a.k_map.nblocks > 1)
+                          ? a.k_map.nblocks * (a.k_map.rows_per_block / TILE)
+                          : (a.nk + TILE - 1) / TILE;
+  dim3 grid(k_tiles, a.bh);
+  bwd128_kernel<<<grid, THREADS, SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+  return check_launch("bwd128_kernel");
+}
+
+}  // namespace a2d

@@ -253,3 +253,14 @@ def test_backward_blocked_cyclic_maps(ops, pr, pc):
     assert rel_fro(dq[live], qf.grad[live]) < REL_TOL
     assert rel_fro(dk, kf.grad) < REL_TOL
     assert rel_fro(dv, vf.grad) < REL_TOL
+
+
+@pytest.mark.parametrize("b_mn", [False, True])
+def test_umma_a_operand_from_tmem(ops, b_mn):
+    """tcgen05.mma with A in TMEM (bf16 pairs per 32-bit column)."""
+    a = uniform((128, 128), 3)
+    b = uniform((128, 128), 4)
+    d = ops.selftest_umma(a, b, 2 | int(b_mn))
+    want = a.float() @ (b.float() if b_mn else b.float().T)
+    torch.cuda.synchronize()
+    assert max_abs(d, want) < 1e-3, max_abs(d, want)
