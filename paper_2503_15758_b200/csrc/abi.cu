@@ -99,6 +99,26 @@ int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, l
   return A2D_OK;
 }
 
+// Same accumulator, box h x box_rows x 1 without swizzle (row-major staging).
+int make_map_f32_dq_flat(CUtensorMap* m, const float* ptr, int h, int rows, int bh,
+                         long long s_row, long long s_bh, int box_rows) {
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) return set_error(A2D_EINVAL, "dq_acc must be 16-byte aligned");
+  if ((s_row * 4) % 16 || (s_bh * 4) % 16)
+    return set_error(A2D_EINVAL, "dq_acc strides must be multiples of 4 elements");
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return set_error(A2D_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)h, (cuuint64_t)rows, (cuuint64_t)bh};
+  cuuint64_t strides[2] = {(cuuint64_t)(s_row * 4), (cuuint64_t)(s_bh * 4)};
+  if (bh == 1) strides[1] = (cuuint64_t)((long long)rows * s_row * 4);
+  cuuint32_t box[3] = {(cuuint32_t)h, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(A2D_ECUDA, "cuTensorMapEncodeTiled(dq_acc flat) failed: %d", (int)r);
+  return A2D_OK;
+}
+
 namespace {
 
 int check_map(const a2d_index_map& m, int n, const char* name) {

@@ -27,6 +27,8 @@ int launch_bwd_finalize(const float* dq_acc, long long asbh, long long asrow, vo
                         float scale, cudaStream_t stream);
 int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, long long s_row,
                     long long s_bh, int box_rows);
+int make_map_f32_dq_flat(CUtensorMap* m, const float* ptr, int h, int rows, int bh,
+                         long long s_row, long long s_bh, int box_rows);
 int bwd_q_tile_rows(int h);
 int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                   const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream);

@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_KV), 1);
-    mbar_init(bar(B_QFULL0), 1);
-    mbar_init(bar(B_QFULL1), 1);
+    mbar_init(bar(B_QFULL0), 2);  // TMA bytes + the producer's stats arrival
+    mbar_init(bar(B_QFULL1), 2);
     mbar_init(bar(B_QEMPTY0), 1);
     mbar_init(bar(B_QEMPTY1), 1);
     mbar_init(bar(B_DOFULL), 1);
@@ -116,11 +116,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       TileCursor cur;
-      cur.start(qr);
+      cur.start(qr, kt_idx);
       for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
         const int qrow = cur.row0(p.q_map);
         const int qs = i & 1;
         mbar_wait(bar(B_QEMPTY0 + qs), ((i >> 1) & 1) ^ 1);
+        if (lane == 0) {  // bulk copy first; the stats' global-load latency overlaps it
+          mbar_expect_tx(bar(B_QFULL0 + qs), TILE_B);
+          for (int s = 0; s < 2; ++s)
+            tma_load_3d(sb + OFF_Q + qs * TILE_B + s * SLAB, &tm_q, bar(B_QFULL0 + qs), s * 64,
+                        qrow, bh);
+        }
         float* s_lse = stat + qs * 256;
         float* s_del = s_lse + 128;
         for (int r = lane; r < 128; r += 32) {
@@ -136,10 +142,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncwarp();
         if (lane == 0) {
-          mbar_expect_tx(bar(B_QFULL0 + qs), TILE_B);
-          for (int s = 0; s < 2; ++s)
-            tma_load_3d(sb + OFF_Q + qs * TILE_B + s * SLAB, &tm_q, bar(B_QFULL0 + qs), s * 64,
-                        qrow, bh);
+          mbar_arrive(bar(B_QFULL0 + qs));
           mbar_wait(bar(B_DOEMPTY), (i & 1) ^ 1);
           mbar_expect_tx(bar(B_DOFULL), TILE_B);
           for (int s = 0; s < 2; ++s)
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const float sl2 = p.scale * kLog2e;
     const bool row_ok = jj < kt.nvalid;
     TileCursor cur;
-    cur.start(qr);
+    cur.start(qr, kt_idx);
     for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
       const int qs = i & 1;
       const TileRef qt = tile_ref(p.q_map, p.nq, cur.row0(p.q_map), TILE);
@@ -356,10 +359,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int quarter = warp & 3;
     const int h = quarter * 32 + lane;  // TMEM lane = head dim of dQ^T
     const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-    const int hc = (h & 31) >> 2, he = (h & 3) * 4;
     int round = 0;
     TileCursor cur;
-    cur.start(qr);
+    cur.start(qr, kt_idx);
     for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
       const int qrow = cur.row0(p.q_map);
       mbar_wait(bar(B_DQFULL), i & 1);
@@ -379,19 +381,20 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t buf = sb + OFF_DQ + (round & 1) * STG;
           if (h == 0) bulk_wait_group_read<1>();  // this buffer's previous reduce has read it
           named_bar_sync(1, 128);
-          const uint32_t slab = buf + (h >> 5) * (32 * 128);
+          // row-major [32 q][128 h] fp32: a warp's 32 head dims are one 128 B row
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
-            const uint32_t addr = slab + q * 128 + ((hc ^ (q & 7)) << 4) + he;
+            const uint32_t addr = buf + q * 512 + h * 4;
             asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v[32 * r2 + q]) : "memory");
           }
           fence_proxy_async_smem();
           named_bar_sync(1, 128);
+#ifdef A2D_X_NO_DQ
+          if (false) {
+#else
           if (h == 0) {
-#pragma unroll
-            for (int s = 0; s < 4; ++s)
-              tma_reduce_add_3d_g(&tm_dq, buf + s * (32 * 128), s * 32,
-                                  qrow + 64 * half + 32 * r2, bh);
+#endif
+            tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + 64 * half + 32 * r2, bh);
             bulk_commit_group();
           }
         }
@@ -422,7 +425,7 @@ int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUten
     configured[dev & 63] = true;
   }
   CUtensorMap tdq;
-  int rc = make_map_f32_dq(&tdq, a.dq_acc, 128, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh, 32);
+  int rc = make_map_f32_dq_flat(&tdq, a.dq_acc, 128, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh, 32);
   if (rc) return rc;
   const int k_tiles = (a.k_map.mode == A2D_IDX_AFFINE && a.k_map.nblocks > 1)
                           ? a.k_map.nblocks * (a.k_map.rows_per_block / TILE)

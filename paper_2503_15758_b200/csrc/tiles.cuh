@@ -146,18 +146,38 @@ __device__ __forceinline__ void query_range(const a2d_index_map& qm, int nq, boo
   }
 }
 
-// Cursor over a TileRange; yields the local row0 of each tile in order.
+// Cursor over a TileRange; yields the local row0 of each tile, cyclically
+// starting at flat position `rot` (callers iterate exactly `total` tiles).
+// Rotating the start per CTA keeps co-resident CTAs of one head on
+// different tiles, so their loads and dQ reduce-adds do not pile onto the
+// same L2 lines at the same time.
 struct TileCursor {
   int b, t;
-  __device__ __forceinline__ void start(const TileRange& r) {
+  __device__ __forceinline__ void start(const TileRange& r, int rot = 0) {
     b = 0;
     t = r.first[0];
     skip(r);
+    if (r.total > 0 && rot > 0) {
+      rot %= r.total;
+      while (rot > 0) {  // jump whole blocks, then within the block
+        const int left = r.last[b] - t;
+        if (rot < left) {
+          t += rot;
+          rot = 0;
+        } else {
+          rot -= left;
+          t = r.last[b];
+          skip(r);
+        }
+      }
+    }
   }
   __device__ __forceinline__ void skip(const TileRange& r) {
-    while (b < r.nblk && t >= r.last[b]) {
+    while (t >= r.last[b]) {
       ++b;
-      if (b < r.nblk) t = r.first[b];
+      if (b >= r.nblk) b = 0;
+      t = r.first[b];
+      if (r.total == 0) return;
     }
   }
   __device__ __forceinline__ void next(const TileRange& r) {

@@ -1,0 +1,38 @@
+#!/bin/bash
+# Build xlib/lib_TRACE.so: bwd128 with clock64 timestamps for one CTA (blockIdx TX,TY).
+set -e
+TX=${1:-3}; TY=${2:-5}
+R=/root/repo/paper_2503_15758_b200/csrc
+rm -rf /tmp/xt && mkdir -p /tmp/xt && cp $R/*.cu $R/*.cuh $R/*.h /tmp/xt/
+sed -i 's|../../include/attn2d_b200.h|/root/repo/include/attn2d_b200.h|' /tmp/xt/*
+python3 - <<'PY'
+p='/tmp/xt/tile_bwd128.cu'; s=open(p).read()
+ev = [("mbar_wait(bar(B_QEMPTY0 + qs), ((i >> 1) & 1) ^ 1);", 0, 0, 'after'),
+      ("tma_load_3d(sb + OFF_DO + s * SLAB, &tm_do, bar(B_DOFULL), s * 64, qrow, bh);", 1, 0, 'after'),
+      ("mbar_wait(bar(B_DOFULL), i & 1);", 2, 1, 'after'),
+      ("mbar_wait(bar(B_PREADY), i & 1);", 3, 1, 'after'),
+      ("mbar_wait(bar(B_DSREADY), i & 1);", 4, 1, 'after'),
+      ("mbar_wait(bar(B_QFULL0 + (qs ^ 1)), ((i + 1) >> 1) & 1);", 5, 1, 'after'),
+      ("mbar_wait(bar(B_DQFREE), (i - 1) & 1);", 6, 1, 'after'),
+      ("mbar_wait(bar(B_QFULL0 + qs), (i >> 1) & 1);", 7, 2, 'after'),
+      ("mbar_wait(bar(B_SFULL), i & 1);", 8, 2, 'after'),
+      ("mbar_arrive(bar(B_PREADY));", 9, 2, 'before'),
+      ("mbar_wait(bar(B_DPFULL), i & 1);", 10, 2, 'after'),
+      ("if (i > 0) mbar_wait(bar(B_DSFREE), (i - 1) & 1);", 11, 2, 'after'),
+      ("mbar_arrive(bar(B_DSREADY));", 12, 2, 'before'),
+      ("mbar_wait(bar(B_DQFULL), i & 1);", 13, 10, 'after'),
+      ("mbar_arrive(bar(B_DQFREE));", 14, 10, 'before'),
+      ("bulk_commit_group();", 15, 12, 'after')]
+for pat, e, w, where in ev:
+    assert pat in s, pat
+    t = f"TRACE({e}, i, {w});"
+    s = s.replace(pat, (pat + " " + t) if where == 'after' else (t + " " + pat), 1)
+s = s.replace('#include "kernels.h"\n', '''#include "kernels.h"
+__device__ long long g_trace[16][1024];
+#define TRACE(ev, i, w) do { if (blockIdx.x == TX && blockIdx.y == TY && warp == (w) && (threadIdx.x & 31) == 0 && (i) < 1024) g_trace[ev][i] = clock64(); } while (0)
+extern "C" int a2d_trace_dump(long long* host) { return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace)); }
+''', 1)
+open(p,'w').write(s)
+PY
+cd /tmp/xt && /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -DTX=$TX -DTY=$TY $XFLAGS -shared -o /root/repo/xlib/lib_TRACE$XSUF.so abi.cu tile_fwd.cu tile_bwd.cu tile_bwd128.cu lse_merge.cu selftest.cu -lcudart_static -lrt -ldl -lpthread
+echo built
