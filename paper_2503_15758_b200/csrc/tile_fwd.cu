@@ -51,16 +51,16 @@ struct FwdLayout {
   static constexpr int SLAB = TILE * 128;  // bytes of one 128-row x 64-col bf16 slab
   static constexpr int SLABS = HD / 64;
   static constexpr int TILE_BYTES = SLAB * SLABS;
-  static constexpr int KST = 2;
-  static constexpr int VST = 2;
-  static constexpr int OFF_Q = 0;
+  static constexpr int KST = 3;
+  static constexpr int VST = 3;
+  static constexpr int OFF_Q = 0;  // Q staging (moved into TMEM before the sweep)
   static constexpr int OFF_K = OFF_Q + TILE_BYTES;
   static constexpr int OFF_V = OFF_K + KST * TILE_BYTES;
-  static constexpr int OFF_P = OFF_V + VST * TILE_BYTES;
-  static constexpr int OFF_BAR = OFF_P + 2 * SLAB;
+  static constexpr int OFF_BAR = OFF_V + VST * TILE_BYTES;
   // barriers
   static constexpr int B_Q = 0;
-  static constexpr int B_KFULL = 1;
+  static constexpr int B_QREADY = 1;
+  static constexpr int B_KFULL = 2;
   static constexpr int B_KEMPTY = B_KFULL + KST;
   static constexpr int B_VFULL = B_KEMPTY + KST;
   static constexpr int B_VEMPTY = B_VFULL + VST;
@@ -69,23 +69,27 @@ struct FwdLayout {
   static constexpr int B_PVDONE = B_PFULL + 1;
   static constexpr int NBAR = B_PVDONE + 1;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
-  static constexpr int BYTES = OFF_TMEMPTR + 16;
-  static constexpr int SMEM = BYTES + 1024;  // slack for 1024-B alignment
+  static constexpr int SMEM = OFF_TMEMPTR + 16;
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
+// TMEM (512 columns): S / P double buffer, O accumulator, Q (bf16 pairs, the
+// A operand of S = Q K^T).  P overwrites the first half of its S buffer and
+// feeds O += P V as the TMEM A operand, so neither Q nor P costs shared-memory
+// bandwidth: per key tile the tensor core reads only K and V from SMEM.
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t TM_S = 0;    // S[b] at b*128
+constexpr uint32_t TM_S = 0;    // S[b] at b*128 (P[b] in its first 64 columns)
 constexpr uint32_t TM_O = 256;
+constexpr uint32_t TM_Q = 384;
 
 template <int HD>
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ a2d_tile_fwd_args p) {
   using L = FwdLayout<HD>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sb = smem_u32(smem);
+  if ((sb & 1023) != 0) __trap();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // q tiles vary fastest so co-resident CTAs share one head's K/V in L2;
@@ -96,6 +100,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar(L::B_Q), 1);
+    mbar_init(bar(L::B_QREADY), 128);
     for (int i = 0; i < L::KST; ++i) {
       mbar_init(bar(L::B_KFULL + i), 1);
       mbar_init(bar(L::B_KEMPTY + i), 1);
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       for (int s = 0; s < L::SLABS; ++s)
         tma_load_3d(sb + L::OFF_Q + s * L::SLAB, &tm_q, bar(L::B_Q), s * 64, qt.row0, bh);
       TileCursor cur;
-      cur.start(kr);
+      cur.start(kr, qt_idx);
       int ks = 0, kph = 0, vs = 0, vph = 0;
       for (int j = 0; j < n_tiles; ++j, cur.next(kr)) {
         const int krow = cur.row0(p.k_map);
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, HD, 0, 1);
       int ks = 0, kph = 0, vs = 0, vph = 0;
-      mbar_wait(bar(L::B_Q), 0);
+      mbar_wait(bar(L::B_QREADY), 0);  // Q is in TMEM
       tc_fence_after();
       auto issue_qk = [&](int j) {
         mbar_wait(bar(L::B_KFULL + ks), kph);
@@ -171,8 +176,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * L::SLAB + (kk & 3) * 32;
-          umma_bf16(d, make_sdesc(sb + L::OFF_Q + off, 16, 1024), make_sdesc(kbase + off, 16, 1024),
-                    idesc_qk, kk > 0);
+          umma_bf16_ts(d, tmem + TM_Q + kk * 8, make_sdesc(kbase + off, 16, 1024), idesc_qk,
+                       kk > 0);
         }
         umma_commit(bar(L::B_KEMPTY + ks));
         umma_commit(bar(L::B_SFULL + (j & 1)));
@@ -185,11 +190,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         mbar_wait(bar(L::B_VFULL + vs), vph);
         tc_fence_after();
         const uint32_t vbase = sb + L::OFF_V + vs * L::TILE_BYTES;
+        const uint32_t pcol = tmem + TM_S + (j & 1) * 128;  // P_j (bf16 pairs) in TMEM
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk) {
-          const uint64_t a = make_sdesc(sb + L::OFF_P + (kk >> 2) * L::SLAB + (kk & 3) * 32, 16, 1024);
           const uint64_t b = make_sdesc(vbase + kk * 2048, L::SLAB, 1024);
-          umma_bf16(tmem + TM_O, a, b, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + TM_O, pcol + kk * 8, b, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(bar(L::B_VEMPTY + vs));
         umma_commit(bar(L::B_PVDONE));
@@ -204,8 +209,32 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const float sl2 = p.scale * kLog2e;
     float m_run = -INFINITY;  // running max of scale*log2e*s
     float l_run = 0.f;
+    if (n_tiles > 0) {
+      // Q row -> TMEM (the A operand of S = Q K^T): the TMA-staged, 128B-swizzled
+      // K-major row is re-read as bf16 pairs, one 32-bit TMEM column per pair.
+      mbar_wait(bar(L::B_Q), 0);
+      uint32_t qv[HD / 2];
+#pragma unroll
+      for (int s = 0; s < L::SLABS; ++s) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 u = *reinterpret_cast<const uint4*>(
+              smem + L::OFF_Q + s * L::SLAB + row * 128 + ((c ^ (row & 7)) << 4));
+          qv[32 * s + 4 * c + 0] = u.x;
+          qv[32 * s + 4 * c + 1] = u.y;
+          qv[32 * s + 4 * c + 2] = u.z;
+          qv[32 * s + 4 * c + 3] = u.w;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c)
+        tmem_st32(tmem + lane_addr + TM_Q + 32 * c, reinterpret_cast<const float*>(qv + 32 * c));
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar(L::B_QREADY));
+    }
     TileCursor cur;
-    cur.start(kr);
+    cur.start(kr, qt_idx);
     for (int j = 0; j < (XLOOP ? n_tiles : 0); ++j, cur.next(kr)) {
       const TileRef kt = tile_ref(p.k_map, p.nk, cur.row0(p.k_map));
       const PairMask pm = pair_mask(p.q_map, qt, kt, causal);
@@ -258,31 +287,28 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const float2 a = fadd2(a01, a23);
       l_run = l_run * alpha + (a.x + a.y);
 
-      // P buffer and O are free once PV_{j-1} has completed.
-      if (j > 0) {
+      // P_j (bf16 pairs) over the first 64 columns of its own S buffer: the
+      // S values there were consumed above, and PV_{j-2} (the last reader of
+      // this buffer's previous P) completed before QK_j was issued.
+      const uint32_t pcol = tmem + lane_addr + TM_S + (j & 1) * 128;
+      tmem_st32(pcol, reinterpret_cast<const float*>(pk));
+      tmem_st32(pcol + 32, reinterpret_cast<const float*>(pk + 32));
+      // O is rescaled only when the running max moved: that needs PV_{j-1}
+      // to have landed in O first.
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
         mbar_wait(bar(L::B_PVDONE), (j - 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
-            float o[32];
-            tmem_ld32(tmem + lane_addr + TM_O + c * 32, o);
-            tmem_wait_ld();
+        for (int c = 0; c < HD / 32; ++c) {
+          float o[32];
+          tmem_ld32(tmem + lane_addr + TM_O + c * 32, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] *= alpha;
-            tmem_st32(tmem + lane_addr + TM_O + c * 32, o);
-          }
-          tmem_wait_st();
+          for (int i = 0; i < 32; ++i) o[i] *= alpha;
+          tmem_st32(tmem + lane_addr + TM_O + c * 32, o);
         }
       }
-      // P (bf16) -> shared, K-major 128B-swizzled: row `row`, 16 chunks of 16 B.
-      const uint32_t prow = sb + L::OFF_P + row * 128;
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        const uint32_t addr = prow + (cc >> 3) * L::SLAB + (((cc & 7) ^ (row & 7)) << 4);
-        st_shared_v4(addr, pk[cc * 4 + 0], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
-      }
-      fence_proxy_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(bar(L::B_PFULL));
     }

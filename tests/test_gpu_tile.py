@@ -124,12 +124,13 @@ def test_forward_blocked_cyclic_maps(ops, pr, pc):
     assert torch.equal(fin, torch.isfinite(lse))
     assert rel_fro(o[fin], want_o[fin]) < REL_TOL
     assert max_abs(lse[fin], want_lse[fin]) < LSE_TOL
-    # the same maps through the array path agree (the array path evaluates
-    # every exponential on MUFU, the affine path offloads a quarter of them
-    # to the cubic exp2 on the FMA pipe: 1e-4 relative)
+    # the same maps through the array path agree up to bf16 rounding of P:
+    # the array path evaluates every exponential on MUFU and visits the key
+    # tiles in another order (another stale running max), the affine path
+    # offloads a quarter of the exponentials to the cubic exp2
     o2, lse2 = ops.tile_forward(q, k, v, causal=True, scale=h ** -0.5, q_index=qi.as_array("cuda"),
                                 k_index=ki.as_array("cuda"))
-    assert max_abs(o2, o) < 5e-4 and max_abs(lse2[fin], lse[fin]) < 5e-4
+    assert max_abs(o2, o) < 5e-3 and max_abs(lse2[fin], lse[fin]) < 5e-4
 
 
 def test_forward_continuation(ops):
