@@ -169,6 +169,11 @@ int a2d_selftest_umma(const void* a, const void* b, float* d, int32_t n,
 int a2d_bench_umma(int32_t variant, int32_t iters, int64_t* cycles_out, int32_t ctas,
                    void* stream);
 
+/* Diagnostic: fill shared memory (mode bit 0) and TMEM (bit 1) of every SM
+ * with NaN patterns, to prove the kernels never consume on-chip memory they
+ * did not write. */
+int a2d_debug_poison(int32_t mode, void* stream);
+
 int a2d_abi_version(void);
 const char* a2d_last_error(void);
 int a2d_num_sms(void);

@@ -25,7 +25,7 @@ F32, BF16 = 0, 1
 
 # every symbol include/attn2d_b200.h declares
 EXPORTS = ("a2d_tile_fwd", "a2d_bwd_preprocess", "a2d_tile_bwd", "a2d_bwd_finalize",
-           "a2d_lse_merge", "a2d_selftest_umma", "a2d_bench_umma", "a2d_abi_version", "a2d_last_error",
+           "a2d_lse_merge", "a2d_selftest_umma", "a2d_bench_umma", "a2d_debug_poison", "a2d_abi_version", "a2d_last_error",
            "a2d_num_sms")
 
 
@@ -86,6 +86,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
                                   c_int32, c_int64, c_void_p, c_int32, c_int64, c_void_p,
                                   c_void_p]
     lib.a2d_bench_umma.argtypes = [c_int32, c_int32, c_void_p, c_int32, c_void_p]
+    lib.a2d_debug_poison.argtypes = [c_int32, c_void_p]
     lib.a2d_selftest_umma.argtypes = [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p]
     lib.a2d_last_error.restype = ctypes.c_char_p
     for name in EXPORTS:

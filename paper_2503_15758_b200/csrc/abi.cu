@@ -249,6 +249,13 @@ int a2d_lse_merge(const float* o_parts, const float* lse_parts, int32_t k_parts,
                           static_cast<cudaStream_t>(stream));
 }
 
+int a2d_debug_poison(int32_t mode, void* stream) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return launch_poison(mode, sms, static_cast<cudaStream_t>(stream));
+}
+
 int a2d_bench_umma(int32_t variant, int32_t iters, int64_t* cycles_out, int32_t ctas, void* stream) {
   return launch_bench_umma(variant, iters, reinterpret_cast<long long*>(cycles_out), ctas,
                            static_cast<cudaStream_t>(stream));

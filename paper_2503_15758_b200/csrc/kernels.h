@@ -32,6 +32,7 @@ int make_map_f32_dq_flat(CUtensorMap* m, const float* ptr, int h, int rows, int 
 int bwd_q_tile_rows(int h);
 int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                   const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream);
+int launch_poison(int mode, int num_sms, cudaStream_t stream);
 int launch_bench_umma(int variant, int iters, long long* out, int ctas, cudaStream_t stream);
 int launch_selftest_umma(const void* a, const void* b, float* d, int n, int b_mn_major,
                          cudaStream_t stream);

@@ -24,52 +24,66 @@ __device__ __forceinline__ float4 ld_stream_f4(const float* p) {
   return v;
 }
 
+// Every load of a row group is issued before the first use: the K partial
+// LSEs (warp-uniform broadcast loads) and the K x RPW float4 slices of O are
+// independent, so each lane keeps K*RPW 16-byte loads in flight instead of
+// waiting on the LSE before touching O.
+template <int K, int RPW>
 __global__ void __launch_bounds__(256) lse_merge_kernel(
     const float* __restrict__ o_parts, const float* __restrict__ lse_parts, int k,
     long long pso, long long psl, long long rows, int h, long long rs, void* __restrict__ o_out,
     int out_dtype, long long out_rs, float* __restrict__ lse_out) {
-  const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long row0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW;
   const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  float w[kMaxParts];
-  float mx = -INFINITY;
-#pragma unroll
-  for (int c = 0; c < kMaxParts; ++c) {
-    w[c] = (c < k) ? __ldg(lse_parts + c * psl + row) : -INFINITY;
-    mx = fmaxf(mx, w[c]);
-  }
-  float tot = 0.f;
-#pragma unroll
-  for (int c = 0; c < kMaxParts; ++c) {
-    w[c] = (mx == -INFINITY || w[c] == -INFINITY) ? 0.f : __expf(w[c] - mx);
-    tot += w[c];
-  }
-  const float inv = tot > 0.f ? 1.f / tot : 0.f;
+  if (row0 >= rows) return;
+  const int kk = K > 0 ? K : k;
   for (int e = lane * 4; e < h; e += 128) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 v[K > 0 ? K : kMaxParts][RPW];
+    float l[K > 0 ? K : kMaxParts][RPW];
 #pragma unroll
-    for (int c = 0; c < kMaxParts; ++c) {
-      if (c < k && w[c] != 0.f) {
-        const float4 v = ld_stream_f4(o_parts + c * pso + row * rs + e);
-        acc.x += w[c] * v.x;
-        acc.y += w[c] * v.y;
-        acc.z += w[c] * v.z;
-        acc.w += w[c] * v.w;
+    for (int c = 0; c < (K > 0 ? K : kMaxParts); ++c) {
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const long long row = row0 + r;
+        const bool ok = c < kk && row < rows;
+        l[c][r] = ok ? __ldg(lse_parts + c * psl + row) : -INFINITY;
+        v[c][r] = ok ? ld_stream_f4(o_parts + c * pso + row * rs + e) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
-    acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
-    if (out_dtype == A2D_F32) {
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(o_out) + row * out_rs + e) = acc;
-    } else {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y);
-      __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z, acc.w);
-      uint2 u;
-      u.x = *reinterpret_cast<uint32_t*>(&lo);
-      u.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o_out) + row * out_rs + e) = u;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const long long row = row0 + r;
+      if (row >= rows) break;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < (K > 0 ? K : kMaxParts); ++c) mx = fmaxf(mx, l[c][r]);
+      float tot = 0.f;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < (K > 0 ? K : kMaxParts); ++c) {
+        // an empty partial (lse = -inf) contributes exactly nothing, whatever its O holds
+        const float w = (mx == -INFINITY || l[c][r] == -INFINITY) ? 0.f : __expf(l[c][r] - mx);
+        tot += w;
+        acc.x = w != 0.f ? fmaf(w, v[c][r].x, acc.x) : acc.x;
+        acc.y = w != 0.f ? fmaf(w, v[c][r].y, acc.y) : acc.y;
+        acc.z = w != 0.f ? fmaf(w, v[c][r].z, acc.z) : acc.z;
+        acc.w = w != 0.f ? fmaf(w, v[c][r].w, acc.w) : acc.w;
+      }
+      const float inv = tot > 0.f ? 1.f / tot : 0.f;
+      acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      if (out_dtype == A2D_F32) {
+        __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(o_out) + row * out_rs + e), acc);
+      } else {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z, acc.w);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&lo);
+        u.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o_out) + row * out_rs + e) = u;
+      }
+      if (lane == 0 && e == 0) lse_out[row] = tot > 0.f ? mx + __logf(tot) : -INFINITY;
     }
   }
-  if (lane == 0) lse_out[row] = tot > 0.f ? mx + __logf(tot) : -INFINITY;
 }
 
 __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
@@ -135,10 +149,20 @@ int launch_lse_merge(const float* o_parts, const float* lse_parts, int k_parts,
                      float* lse_out, cudaStream_t stream) {
   if (rows == 0) return A2D_OK;
   const int warps = 8;
-  const long long blocks = (rows + warps - 1) / warps;
-  lse_merge_kernel<<<(unsigned)blocks, warps * 32, 0, stream>>>(
-      o_parts, lse_parts, k_parts, part_stride_o, part_stride_lse, rows, h, row_stride, o_out,
-      out_dtype, out_row_stride, lse_out);
+  auto go = [&](auto kern, int rpw) {
+    const long long blocks = (rows + warps * rpw - 1) / (warps * rpw);
+    kern<<<(unsigned)blocks, warps * 32, 0, stream>>>(o_parts, lse_parts, k_parts, part_stride_o,
+                                                     part_stride_lse, rows, h, row_stride, o_out,
+                                                     out_dtype, out_row_stride, lse_out);
+  };
+  switch (k_parts) {
+    case 1: go(lse_merge_kernel<1, 4>, 4); break;
+    case 2: go(lse_merge_kernel<2, 4>, 4); break;
+    case 3: go(lse_merge_kernel<3, 2>, 2); break;
+    case 4: go(lse_merge_kernel<4, 2>, 2); break;
+    case 8: go(lse_merge_kernel<8, 1>, 1); break;
+    default: go(lse_merge_kernel<0, 1>, 1); break;
+  }
   return check_launch("lse_merge_kernel");
 }
 

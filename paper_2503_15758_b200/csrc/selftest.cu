@@ -200,7 +200,50 @@ __global__ void __launch_bounds__(128, 1) umma_bench_kernel(int variant, int ite
   }
 }
 
+// Fills shared memory and all 512 TMEM columns of every SM with NaN bit
+// patterns, so a later kernel that consumes on-chip memory it never wrote
+// shows up as NaNs instead of passing by luck (tests/test_gpu_tile.py).
+__global__ void __launch_bounds__(128, 1) poison_kernel(int mode, int smem_bytes) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (mode & 1) {
+    for (int i = threadIdx.x * 16; i < smem_bytes; i += blockDim.x * 16)
+      *reinterpret_cast<uint4*>(smem + i) = make_uint4(0x7fc07fc0u, 0x7fc07fc0u, 0x7fc07fc0u, 0x7fc07fc0u);
+  }
+  __syncthreads();
+  if (mode & 2) {
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+      tmem_alloc(smem_u32(&slot), 512);
+      tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(0x7fc00000u);
+    for (int c = 0; c < 512; c += 32) tmem_st32(tmem + (uint32_t(warp * 32) << 16) + c, v);
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tc_fence_after();
+      tmem_dealloc(tmem, 512);
+    }
+  }
+}
+
 }  // namespace
+
+int launch_poison(int mode, int num_sms, cudaStream_t stream) {
+  const int smem = 227 * 1024 - 1024;  // leaves room for the static TMEM slot
+  cudaError_t e = cudaFuncSetAttribute(poison_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(poison)");
+  poison_kernel<<<num_sms * 2, 128, smem, stream>>>(mode, smem);
+  return check_launch("poison_kernel");
+}
 
 int launch_bench_umma(int variant, int iters, long long* out, int ctas, cudaStream_t stream) {
   const int smem = 2 * 65536 + 64 + 1024;

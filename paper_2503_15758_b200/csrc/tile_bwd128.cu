@@ -48,7 +48,7 @@ enum {
 constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
 constexpr int SMEM = OFF_TMEMPTR + 16;
 static_assert(SMEM <= 232448, "shared memory budget");
-constexpr uint32_t TM_DV = 0, TM_DK = 128, TM_X = 256, TM_DQ = 384;
+constexpr uint32_t TM_DV = 0, TM_DK = 128, TM_X = 256, TM_Y = 384;
 
 __global__ void __launch_bounds__(THREADS, 1)
     bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -161,15 +161,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         return make_sdesc(base + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
       };
       auto mnmaj = [](uint32_t base, int kk) { return make_sdesc(base + kk * 2048, SLAB, 1024); };
-      auto issue_s = [&](uint32_t a_base, uint32_t b_base) {
+      auto issue_s = [&](uint32_t col, uint32_t a_base, uint32_t b_base) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_bf16(tmem + TM_X, kmaj(a_base, kk), kmaj(b_base, kk), id_ss, kk > 0);
+          umma_bf16(tmem + col, kmaj(a_base, kk), kmaj(b_base, kk), id_ss, kk > 0);
       };
       mbar_wait(bar(B_KV), 0);
       mbar_wait(bar(B_QFULL0), 0);
       tc_fence_after();
-      issue_s(sb + OFF_K, sb + OFF_Q);
+      issue_s(TM_X, sb + OFF_K, sb + OFF_Q);
       umma_commit(bar(B_SFULL));
       for (int i = 0; i < n_tiles; ++i) {
         const int qs = i & 1;
@@ -182,32 +182,32 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kk = 0; kk < 8; ++kk)
           umma_bf16_ts(tmem + TM_DV, tmem + TM_X + (kk >> 2) * 64 + (kk & 3) * 8,
                        mnmaj(sb + OFF_DO, kk), id_kmn, (i > 0 || kk > 0));
-        // dP^T = V dO_i^T overwrites X after dV has read P^T (in-order pipe)
-        issue_s(sb + OFF_V, sb + OFF_DO);
-        umma_commit(bar(B_DOEMPTY));
-        umma_commit(bar(B_DPFULL));
-        // once dS_i is out of TMEM, X takes S_{i+1}
-        mbar_wait(bar(B_DSREADY), i & 1);
-        tc_fence_after();
-        if (i + 1 < n_tiles) {
-          mbar_wait(bar(B_QFULL0 + (qs ^ 1)), ((i + 1) >> 1) & 1);
-          tc_fence_after();
-          issue_s(sb + OFF_K, sb + OFF_Q + (qs ^ 1) * TILE_B);
-          umma_commit(bar(B_SFULL));
-        }
-        // dK += dS^T Q_i
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16(tmem + TM_DK, kmaj(sb + OFF_DS, kk), mnmaj(sq, kk), id_kmn, (i > 0 || kk > 0));
-        umma_commit(bar(B_QEMPTY0 + qs));
-        // dQ^T = K^T dS^T once the drain warps have emptied dQ
+        // dP^T = V dO_i^T -> Y, once the drain warps have emptied dQ_{i-1} from it
         if (i > 0) {
           mbar_wait(bar(B_DQFREE), (i - 1) & 1);
           tc_fence_after();
         }
+        issue_s(TM_Y, sb + OFF_V, sb + OFF_DO);
+        umma_commit(bar(B_DOEMPTY));
+        umma_commit(bar(B_DPFULL));
+        // S_{i+1} -> X right away: dV_i has read P_i from X (in-order pipe), so the
+        // exponentials of tile i+1 start while dS_i is still being formed
+        if (i + 1 < n_tiles) {
+          mbar_wait(bar(B_QFULL0 + (qs ^ 1)), ((i + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_s(TM_X, sb + OFF_K, sb + OFF_Q + (qs ^ 1) * TILE_B);
+          umma_commit(bar(B_SFULL));
+        }
+        // dK += dS^T Q_i and dQ^T = K^T dS^T -> Y (dP_i has been read out of Y)
+        mbar_wait(bar(B_DSREADY), i & 1);
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_bf16(tmem + TM_DQ, mnmaj(sb + OFF_K, kk), mnmaj(sb + OFF_DS, kk), id_mnmn, kk > 0);
+          umma_bf16(tmem + TM_DK, kmaj(sb + OFF_DS, kk), mnmaj(sq, kk), id_kmn, (i > 0 || kk > 0));
+        umma_commit(bar(B_QEMPTY0 + qs));
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16(tmem + TM_Y, mnmaj(sb + OFF_K, kk), mnmaj(sb + OFF_DS, kk), id_mnmn, kk > 0);
         umma_commit(bar(B_DSFREE));
         umma_commit(bar(B_DQFULL));
       }
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float dp[32];
-        tmem_ld32(tmem + lane_addr + TM_X + c0 + 32 * h, dp);
+        tmem_ld32(tmem + lane_addr + TM_Y + c0 + 32 * h, dp);
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
@@ -369,8 +369,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         float v[64];
-        tmem_ld32(tmem + lane_addr + TM_DQ + 64 * half, v);
-        tmem_ld32(tmem + lane_addr + TM_DQ + 64 * half + 32, v + 32);
+        tmem_ld32(tmem + lane_addr + TM_Y + 64 * half, v);
+        tmem_ld32(tmem + lane_addr + TM_Y + 64 * half + 32, v + 32);
         tmem_wait_ld();
         if (half == 1) {
           tc_fence_before();

@@ -65,9 +65,9 @@ struct FwdLayout {
   static constexpr int B_VFULL = B_KEMPTY + KST;
   static constexpr int B_VEMPTY = B_VFULL + VST;
   static constexpr int B_SFULL = B_VEMPTY + VST;
-  static constexpr int B_PFULL = B_SFULL + 2;
-  static constexpr int B_PVDONE = B_PFULL + 1;
-  static constexpr int NBAR = B_PVDONE + 1;
+  static constexpr int B_PFULL = B_SFULL + 2;   // 2 barriers: P_j arrives on [j & 1]
+  static constexpr int B_PVDONE = B_PFULL + 2;  // 2 barriers: PV_j arrives on [j & 1]
+  static constexpr int NBAR = B_PVDONE + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
   static constexpr int SMEM = OFF_TMEMPTR + 16;
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   // within a head the heaviest (causal) tiles start first.
   const int bh = blockIdx.y;
   const int qt_idx = gridDim.x - 1 - blockIdx.x;
+  const int rot = qt_idx;  // rotated key sweep (TileCursor)
   auto bar = [&](int i) { return sb + L::OFF_BAR + 8 * i; };
 
   if (threadIdx.x == 0) {
@@ -111,8 +112,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     }
     mbar_init(bar(L::B_SFULL + 0), 1);
     mbar_init(bar(L::B_SFULL + 1), 1);
-    mbar_init(bar(L::B_PFULL), 128);
-    mbar_init(bar(L::B_PVDONE), 1);
+    mbar_init(bar(L::B_PFULL + 0), 128);
+    mbar_init(bar(L::B_PFULL + 1), 128);
+    mbar_init(bar(L::B_PVDONE + 0), 1);
+    mbar_init(bar(L::B_PVDONE + 1), 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       for (int s = 0; s < L::SLABS; ++s)
         tma_load_3d(sb + L::OFF_Q + s * L::SLAB, &tm_q, bar(L::B_Q), s * 64, qt.row0, bh);
       TileCursor cur;
-      cur.start(kr, qt_idx);
+      cur.start(kr, rot);
       int ks = 0, kph = 0, vs = 0, vph = 0;
       for (int j = 0; j < n_tiles; ++j, cur.next(kr)) {
         const int krow = cur.row0(p.k_map);
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       issue_qk(0);
       for (int j = 0; j < n_tiles; ++j) {
         if (j + 1 < n_tiles) issue_qk(j + 1);
-        XWAIT(bar(L::B_PFULL), j & 1);
+        XWAIT(bar(L::B_PFULL + (j & 1)), (j >> 1) & 1);
         mbar_wait(bar(L::B_VFULL + vs), vph);
         tc_fence_after();
         const uint32_t vbase = sb + L::OFF_V + vs * L::TILE_BYTES;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           umma_bf16_ts(tmem + TM_O, pcol + kk * 8, b, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(bar(L::B_VEMPTY + vs));
-        umma_commit(bar(L::B_PVDONE));
+        umma_commit(bar(L::B_PVDONE + (j & 1)));
         if (++vs == L::VST) { vs = 0; vph ^= 1; }
       }
     }
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mbar_arrive(bar(L::B_QREADY));
     }
     TileCursor cur;
-    cur.start(kr, qt_idx);
+    cur.start(kr, rot);
     for (int j = 0; j < (XLOOP ? n_tiles : 0); ++j, cur.next(kr)) {
       const TileRef kt = tile_ref(p.k_map, p.nk, cur.row0(p.k_map));
       const PairMask pm = pair_mask(p.q_map, qt, kt, causal);
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       // O is rescaled only when the running max moved: that needs PV_{j-1}
       // to have landed in O first.
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-        mbar_wait(bar(L::B_PVDONE), (j - 1) & 1);
+        mbar_wait(bar(L::B_PVDONE + ((j - 1) & 1)), ((j - 1) >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
@@ -310,12 +313,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(bar(L::B_PFULL));
+      // a warp whose rows are all masked can reach tile j+1 (S_{j+1} is issued
+      // before PV_j) while another is still on tile j: alternating barriers
+      // keep its early arrival out of tile j's count
+      mbar_arrive(bar(L::B_PFULL + (j & 1)));
     }
 
     // ------------------------------------------------------------ epilogue
     if (n_tiles > 0) {
-      mbar_wait(bar(L::B_PVDONE), (n_tiles - 1) & 1);
+      // PV_j arrives on PVDONE[j & 1], so each barrier sees every other PV and
+      // a parity wait can never alias a phase two steps back: the last PV on
+      // each barrier is awaited exactly.
+      if (n_tiles > 1)
+        mbar_wait(bar(L::B_PVDONE + ((n_tiles - 2) & 1)), ((n_tiles - 2) >> 1) & 1);
+      mbar_wait(bar(L::B_PVDONE + ((n_tiles - 1) & 1)), ((n_tiles - 1) >> 1) & 1);
       tc_fence_after();
     }
     const bool valid = row < qt.nvalid;

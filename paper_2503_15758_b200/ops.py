@@ -324,3 +324,11 @@ def selftest_umma(a: torch.Tensor, b: torch.Tensor, b_mn_major: bool) -> torch.T
     _lib.check(lib.a2d_selftest_umma(a.data_ptr(), b.data_ptr(), d.data_ptr(), n,
                                      int(b_mn_major), _stream(a)), "a2d_selftest_umma")
     return d
+
+
+def debug_poison(mode: int = 3, device=None) -> None:
+    """Diagnostic: fill SMEM (bit 0) and TMEM (bit 1) of every SM with NaNs."""
+    lib = _lib.load()
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    _lib.check(lib.a2d_debug_poison(int(mode), torch.cuda.current_stream(dev).cuda_stream),
+               "a2d_debug_poison")
