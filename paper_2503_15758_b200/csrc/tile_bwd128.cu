@@ -7,20 +7,25 @@
 //
 // One CTA = one 128-key tile of one head; it sweeps 128-query tiles:
 //   S^T  = K Q_i^T            -> TMEM X      (SS, M128 N128)
+//   dP^T = V dO_i^T           -> TMEM Y      (SS; needs no P, so it runs
+//                                             while the exponentials are formed)
 //   P^T  = exp2(S^T c - lse)  -> TMEM X (bf16, in place)          [P/dS warpgroups]
 //   dV  += P^T dO_i           (TS: A from TMEM)                   -> TMEM dV
-//   dP^T = V dO_i^T           -> TMEM X (after dV in pipe order)
+//   S_{i+1} -> X              (X is free once dV_i has read P_i: in-order pipe)
 //   dS^T = P^T (dP^T - delta) -> smem (bf16, 128B swizzle)          [P/dS warpgroups]
+//   dQ^T = K^T dS^T           (SS, both MN-major)                  -> TMEM Y
 //   dK  += dS^T Q_i           (SS)                                 -> TMEM dK
-//   dQ^T = K^T dS^T           (SS, both MN-major)                  -> TMEM dQ
-//   dQ   -> 2 x 16 KB fp32 staging -> TMA bulk reduce-add into dq_acc
-// S_{i+1} is issued as soon as dS_i is out of TMEM, so the exponentials of
-// tile i+1 overlap dK_i and dQ_i on the tensor pipe.
+//   dQ   -> registers (Y free again) -> fp32 staging -> TMA bulk reduce-add
+// Tensor-pipe order per tile: dP_i, dV_i, S_{i+1}, dQ_i, dK_i.  The P/dS
+// warpgroups run P_i then dS_i back to back (dP_i is ready when P_i is), and
+// P_{i+1} overlaps dQ_i / dK_i; the dQ drain empties Y while dK_i runs.
 //
-// TMEM (512 cols): dV [0,128) dK [128,256) X [256,384) dQ^T [384,512).
+// TMEM (512 cols): dV [0,128) dK [128,256) X [256,384) Y [384,512).
 // SMEM (231.6 KB): K, V, 2 x Q, dO, dS^T, 2 x dQ staging, LSE/delta stats.
-// Warps (448 threads): 0 TMA producer, 1 MMA issuer, 2-5 P/dS warpgroup A
-// (query columns 0-63), 6-9 warpgroup B (64-127), 10-13 dQ drain.
+// Warps (512 threads, register budgets via setmaxnreg):
+//   0 TMA producer, 1 MMA issuer, 2-3 idle                         (72 regs)
+//   4-7 P/dS warpgroup A (query columns 0-63), 8-11 B (64-127)     (136 regs)
+//   12-15 dQ drain: all 128 columns of Y in registers at once       (168 regs)
 #include "sm100.cuh"
 #include "tiles.cuh"
 #include "kernels.h"
@@ -29,7 +34,7 @@ namespace a2d {
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int THREADS = 448;
+constexpr int THREADS = 512;
 constexpr int SLAB = 128 * 128;  // 128 rows x 128 B
 constexpr int TILE_B = 2 * SLAB; // one 128 x 128 bf16 tile
 constexpr int OFF_K = 0;
@@ -105,132 +110,155 @@ __global__ void __launch_bounds__(THREADS, 1)
   query_range(p.q_map, p.nq, causal, kt.gmin, qr, TILE);
   const int n_tiles = qr.total;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    if (n_tiles > 0) {
-      if (lane == 0) {
-        mbar_expect_tx(bar(B_KV), 2 * TILE_B);
-        for (int s = 0; s < 2; ++s) {
-          tma_load_3d(sb + OFF_K + s * SLAB, &tm_k, bar(B_KV), s * 64, kt.row0, bh);
-          tma_load_3d(sb + OFF_V + s * SLAB, &tm_v, bar(B_KV), s * 64, kt.row0, bh);
-        }
-      }
-      TileCursor cur;
-      cur.start(qr, kt_idx);
-      for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
-        const int qrow = cur.row0(p.q_map);
-        const int qs = i & 1;
-        mbar_wait(bar(B_QEMPTY0 + qs), ((i >> 1) & 1) ^ 1);
-        if (lane == 0) {  // bulk copy first; the stats' global-load latency overlaps it
-          mbar_expect_tx(bar(B_QFULL0 + qs), TILE_B);
-          for (int s = 0; s < 2; ++s)
-            tma_load_3d(sb + OFF_Q + qs * TILE_B + s * SLAB, &tm_q, bar(B_QFULL0 + qs), s * 64,
-                        qrow, bh);
-        }
-        float* s_lse = stat + qs * 256;
-        float* s_del = s_lse + 128;
-        for (int r = lane; r < 128; r += 32) {
-          const int gr = qrow + r;
-          float l2 = INFINITY, dl = 0.f;
-          if (gr < p.nq) {
-            const float l = p.lse[(long long)bh * p.nq + gr];
-            l2 = (l == -INFINITY) ? INFINITY : l * kLog2e;
-            dl = p.delta[(long long)bh * p.nq + gr];
-          }
-          s_lse[r] = l2;
-          s_del[r] = dl;
-        }
-        __syncwarp();
+  if (warp < 4) {
+    regs_dec<72>();
+    if (warp == 0) {
+      // ---------------------------------------------------------- producer
+      if (n_tiles > 0) {
         if (lane == 0) {
-          mbar_arrive(bar(B_QFULL0 + qs));
-          mbar_wait(bar(B_DOEMPTY), (i & 1) ^ 1);
-          mbar_expect_tx(bar(B_DOFULL), TILE_B);
-          for (int s = 0; s < 2; ++s)
-            tma_load_3d(sb + OFF_DO + s * SLAB, &tm_do, bar(B_DOFULL), s * 64, qrow, bh);
+          mbar_expect_tx(bar(B_KV), 2 * TILE_B);
+          for (int s = 0; s < 2; ++s) {
+            tma_load_3d(sb + OFF_K + s * SLAB, &tm_k, bar(B_KV), s * 64, kt.row0, bh);
+            tma_load_3d(sb + OFF_V + s * SLAB, &tm_v, bar(B_KV), s * 64, kt.row0, bh);
+          }
         }
-        __syncwarp();
+        // the LSE / delta rows of tile i+1 are loaded into registers while tile i
+        // is in flight, so their global-load latency never gates S_{i+1}
+        TileCursor cur;
+        cur.start(qr, kt_idx);
+        float l2n[4], dln[4];
+        auto load_stats = [&](int qrow) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int gr = qrow + lane + 32 * k;
+            l2n[k] = INFINITY;
+            dln[k] = 0.f;
+            if (gr < p.nq) {
+              const float l = p.lse[(long long)bh * p.nq + gr];
+              l2n[k] = (l == -INFINITY) ? INFINITY : l * kLog2e;
+              dln[k] = p.delta[(long long)bh * p.nq + gr];
+            }
+          }
+        };
+        load_stats(cur.row0(p.q_map));
+        for (int i = 0; i < n_tiles; ++i) {
+          const int qrow = cur.row0(p.q_map);
+          const int qs = i & 1;
+          mbar_wait(bar(B_QEMPTY0 + qs), ((i >> 1) & 1) ^ 1);
+          if (lane == 0) {
+            mbar_expect_tx(bar(B_QFULL0 + qs), TILE_B);
+            for (int s = 0; s < 2; ++s)
+              tma_load_3d(sb + OFF_Q + qs * TILE_B + s * SLAB, &tm_q, bar(B_QFULL0 + qs), s * 64,
+                          qrow, bh);
+          }
+          float* s_lse = stat + qs * 256;
+          float* s_del = s_lse + 128;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            s_lse[lane + 32 * k] = l2n[k];
+            s_del[lane + 32 * k] = dln[k];
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(B_QFULL0 + qs));
+          cur.next(qr);
+          if (i + 1 < n_tiles) load_stats(cur.row0(p.q_map));
+          if (lane == 0) {
+            mbar_wait(bar(B_DOEMPTY), (i & 1) ^ 1);
+            mbar_expect_tx(bar(B_DOFULL), TILE_B);
+            for (int s = 0; s < 2; ++s)
+              tma_load_3d(sb + OFF_DO + s * SLAB, &tm_do, bar(B_DOFULL), s * 64, qrow, bh);
+          }
+          __syncwarp();
+        }
+      }
+    } else if (warp == 1) {
+      // ---------------------------------------------------------- MMA issuer
+      if (lane == 0 && n_tiles > 0) {
+        constexpr uint32_t id_ss = make_idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
+        constexpr uint32_t id_kmn = make_idesc_bf16(128, 128, 0, 1);  // P^T dO, dS^T Q
+        constexpr uint32_t id_mnmn = make_idesc_bf16(128, 128, 1, 1); // K^T dS^T
+        auto kmaj = [](uint32_t base, int kk) {
+          return make_sdesc(base + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
+        };
+        auto mnmaj = [](uint32_t base, int kk) { return make_sdesc(base + kk * 2048, SLAB, 1024); };
+        auto issue_s = [&](uint32_t col, uint32_t a_base, uint32_t b_base) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + col, kmaj(a_base, kk), kmaj(b_base, kk), id_ss, kk > 0);
+        };
+        mbar_wait(bar(B_KV), 0);
+        mbar_wait(bar(B_QFULL0), 0);
+        tc_fence_after();
+        issue_s(TM_X, sb + OFF_K, sb + OFF_Q);
+        umma_commit(bar(B_SFULL));
+        for (int i = 0; i < n_tiles; ++i) {
+          const int qs = i & 1;
+          const uint32_t sq = sb + OFF_Q + qs * TILE_B;
+          // dP^T = V dO_i^T -> Y, once the drain has emptied dQ_{i-1} out of it
+          mbar_wait(bar(B_DOFULL), i & 1);
+          if (i > 0) mbar_wait(bar(B_DQFREE), (i - 1) & 1);
+          tc_fence_after();
+          issue_s(TM_Y, sb + OFF_V, sb + OFF_DO);
+          umma_commit(bar(B_DPFULL));
+          // dV += P^T dO_i (P^T in TMEM: warpgroup A's 64 queries at X+0, B's at X+64)
+          mbar_wait(bar(B_PREADY), i & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16_ts(tmem + TM_DV, tmem + TM_X + (kk >> 2) * 64 + (kk & 3) * 8,
+                         mnmaj(sb + OFF_DO, kk), id_kmn, (i > 0 || kk > 0));
+          umma_commit(bar(B_DOEMPTY));
+          // S_{i+1} -> X: dV_i has read P_i out of X (in-order pipe)
+          if (i + 1 < n_tiles) {
+            mbar_wait(bar(B_QFULL0 + (qs ^ 1)), ((i + 1) >> 1) & 1);
+            tc_fence_after();
+            issue_s(TM_X, sb + OFF_K, sb + OFF_Q + (qs ^ 1) * TILE_B);
+            umma_commit(bar(B_SFULL));
+          }
+          // dQ^T = K^T dS^T -> Y (dP_i was read out of Y before dS_i was published),
+          // then dK += dS^T Q_i while the drain empties Y
+          mbar_wait(bar(B_DSREADY), i & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_Y, mnmaj(sb + OFF_K, kk), mnmaj(sb + OFF_DS, kk), id_mnmn, kk > 0);
+          umma_commit(bar(B_DQFULL));
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + TM_DK, kmaj(sb + OFF_DS, kk), mnmaj(sq, kk), id_kmn, (i > 0 || kk > 0));
+          umma_commit(bar(B_QEMPTY0 + qs));
+          umma_commit(bar(B_DSFREE));
+        }
+        umma_commit(bar(B_DONE));
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && n_tiles > 0) {
-      constexpr uint32_t id_ss = make_idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
-      constexpr uint32_t id_kmn = make_idesc_bf16(128, 128, 0, 1);  // P^T dO, dS^T Q
-      constexpr uint32_t id_mnmn = make_idesc_bf16(128, 128, 1, 1); // K^T dS^T
-      auto kmaj = [](uint32_t base, int kk) {
-        return make_sdesc(base + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
-      };
-      auto mnmaj = [](uint32_t base, int kk) { return make_sdesc(base + kk * 2048, SLAB, 1024); };
-      auto issue_s = [&](uint32_t col, uint32_t a_base, uint32_t b_base) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16(tmem + col, kmaj(a_base, kk), kmaj(b_base, kk), id_ss, kk > 0);
-      };
-      mbar_wait(bar(B_KV), 0);
-      mbar_wait(bar(B_QFULL0), 0);
-      tc_fence_after();
-      issue_s(TM_X, sb + OFF_K, sb + OFF_Q);
-      umma_commit(bar(B_SFULL));
-      for (int i = 0; i < n_tiles; ++i) {
-        const int qs = i & 1;
-        const uint32_t sq = sb + OFF_Q + qs * TILE_B;
-        // dV += P^T dO_i (P^T in TMEM: warpgroup A's 64 queries at X+0, B's at X+64)
-        mbar_wait(bar(B_DOFULL), i & 1);
-        mbar_wait(bar(B_PREADY), i & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16_ts(tmem + TM_DV, tmem + TM_X + (kk >> 2) * 64 + (kk & 3) * 8,
-                       mnmaj(sb + OFF_DO, kk), id_kmn, (i > 0 || kk > 0));
-        // dP^T = V dO_i^T -> Y, once the drain warps have emptied dQ_{i-1} from it
-        if (i > 0) {
-          mbar_wait(bar(B_DQFREE), (i - 1) & 1);
-          tc_fence_after();
-        }
-        issue_s(TM_Y, sb + OFF_V, sb + OFF_DO);
-        umma_commit(bar(B_DOEMPTY));
-        umma_commit(bar(B_DPFULL));
-        // S_{i+1} -> X right away: dV_i has read P_i from X (in-order pipe), so the
-        // exponentials of tile i+1 start while dS_i is still being formed
-        if (i + 1 < n_tiles) {
-          mbar_wait(bar(B_QFULL0 + (qs ^ 1)), ((i + 1) >> 1) & 1);
-          tc_fence_after();
-          issue_s(TM_X, sb + OFF_K, sb + OFF_Q + (qs ^ 1) * TILE_B);
-          umma_commit(bar(B_SFULL));
-        }
-        // dK += dS^T Q_i and dQ^T = K^T dS^T -> Y (dP_i has been read out of Y)
-        mbar_wait(bar(B_DSREADY), i & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16(tmem + TM_DK, kmaj(sb + OFF_DS, kk), mnmaj(sq, kk), id_kmn, (i > 0 || kk > 0));
-        umma_commit(bar(B_QEMPTY0 + qs));
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16(tmem + TM_Y, mnmaj(sb + OFF_K, kk), mnmaj(sb + OFF_DS, kk), id_mnmn, kk > 0);
-        umma_commit(bar(B_DSFREE));
-        umma_commit(bar(B_DQFULL));
-      }
-      umma_commit(bar(B_DONE));
-    }
-  } else if (warp < 10) {
+  } else if (warp < 12) {
+    regs_inc<136>();
     // ------------------------------------------------------------ P / dS warpgroups
-    const int wg = (warp - 2) >> 2;  // 0: query columns 0-63, 1: 64-127
+    const int wg = (warp - 4) >> 2;  // 0: query columns 0-63, 1: 64-127
     const int quarter = warp & 3;
     const int jj = quarter * 32 + lane;  // key row within the tile
     const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
     const int c0 = wg * 64;
     const float sl2 = p.scale * kLog2e;
     const bool row_ok = jj < kt.nvalid;
+    const bool affine = p.q_map.mode != A2D_IDX_ARRAY;
+    // causal threshold of query block b against this key tile, ceil((kt.gmin -
+    // base_b) / s): one division per block change instead of one per tile
+    int blk = -1;
+    long long dblk = 0;
     TileCursor cur;
     cur.start(qr, kt_idx);
     for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
       const int qs = i & 1;
-      const TileRef qt = tile_ref(p.q_map, p.nq, cur.row0(p.q_map), TILE);
+      const int qrow0 = cur.row0(p.q_map);
+      const int qend = (!affine || p.q_map.nblocks == 1) ? p.nq : (cur.b + 1) * p.q_map.rows_per_block;
+      const int qvalid = min(TILE, qend - qrow0);
       int first = 0;  // first visible query column of this key row
       bool full = true;
       if (causal) {
-        if (p.q_map.mode == A2D_IDX_ARRAY) {
+        if (!affine) {
+          const TileRef qt = tile_ref(p.q_map, p.nq, qrow0, TILE);
           PairMask pm;
           pm.partial = true;
           pm.thr = 0;
@@ -238,14 +266,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           first = col_first(p.q_map, p.k_map, qt, kt, pm, true, jj);
           full = false;
         } else {
-          long long thr = ceil_div_s(kt.gmin - qt.gmin, p.q_map.stride);
+          if (cur.b != blk) {
+            blk = cur.b;
+            dblk = ceil_div_s(kt.gmin - p.q_map.base[blk], p.q_map.stride);
+          }
+          long long thr = dblk - (long long)TILE * cur.t;
           thr = max(-(long long)(2 * TILE), min((long long)(2 * TILE), thr));
           first = jj + (int)thr;
           full = thr <= -(TILE - 1);
         }
       }
       if (!row_ok) first = TILE;
-      full = full && kt.nvalid == TILE && qt.nvalid == TILE;
+      full = full && kt.nvalid == TILE && qvalid == TILE;
       const float* s_lse = stat + qs * 256 + c0;
       const float* s_del = s_lse + 128;
       mbar_wait(bar(B_QFULL0 + qs), (i >> 1) & 1);  // orders the producer's stats stores
@@ -263,8 +295,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           const float2 x = ffma2(make_float2(pr[c], pr[c + 1]), sc,
                                  make_float2(-s_lse[c], -s_lse[c + 1]));
           const float2 e = (((c >> 1) & 3) == 3) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          pr[c] = e.x;
-          pr[c + 1] = e.y;
           pk[c >> 1] = pack_bf16(e.x, e.y);
         }
       } else {
@@ -274,8 +304,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                                  make_float2(-s_lse[c], -s_lse[c + 1]));
           const float e0 = (c0 + c >= first) ? ex2(x.x) : 0.f;
           const float e1 = (c0 + c + 1 >= first) ? ex2(x.y) : 0.f;
-          pr[c] = e0;
-          pr[c + 1] = e1;
           pk[c >> 1] = pack_bf16(e0, e1);
         }
       }
@@ -288,7 +316,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(bar(B_DPFULL), i & 1);
       tc_fence_after();
       // dS = P (dP - delta), with P re-read from its bf16 pairs (the same
-      // rounded P that fed dV; keeps the warpgroup within 128 registers)
+      // rounded P that fed dV)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float dp[32];
@@ -303,7 +331,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           pk[(32 * h + c) >> 1] = pack_bf16(pf.x * d.x, pf.y * d.y);
         }
       }
-      tc_fence_before();  // the dP^T loads are done before X is handed back
+      tc_fence_before();  // the dP^T loads are done before Y is handed back
       if (i > 0) mbar_wait(bar(B_DSFREE), (i - 1) & 1);
       // dS^T row jj -> K-major SW128 slab `wg` (64 queries = 128 B per row)
       const uint32_t drow = sb + OFF_DS + wg * SLAB + jj * 128;
@@ -355,6 +383,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
+    regs_inc<168>();
     // ------------------------------------------------------------ dQ drain
     const int quarter = warp & 3;
     const int h = quarter * 32 + lane;  // TMEM lane = head dim of dQ^T
@@ -366,37 +395,33 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int qrow = cur.row0(p.q_map);
       mbar_wait(bar(B_DQFULL), i & 1);
       tc_fence_after();
+      // all 128 query columns at once: Y is handed back before any staging
+      float v[128];
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float v[64];
-        tmem_ld32(tmem + lane_addr + TM_Y + 64 * half, v);
-        tmem_ld32(tmem + lane_addr + TM_Y + 64 * half + 32, v + 32);
-        tmem_wait_ld();
-        if (half == 1) {
-          tc_fence_before();
-          mbar_arrive(bar(B_DQFREE));
+      for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_addr + TM_Y + 32 * c, v + 32 * c);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(bar(B_DQFREE));
+#pragma unroll
+      for (int r = 0; r < 4; ++r, ++round) {
+        const uint32_t buf = sb + OFF_DQ + (round & 1) * STG;
+        if (h == 0) bulk_wait_group_read<1>();  // this buffer's previous reduce has read it
+        named_bar_sync(1, 128);
+        // row-major [32 q][128 h] fp32: a warp's 32 head dims are one 128 B row
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const uint32_t addr = buf + q * 512 + h * 4;
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v[32 * r + q]) : "memory");
         }
-#pragma unroll
-        for (int r2 = 0; r2 < 2; ++r2, ++round) {
-          const uint32_t buf = sb + OFF_DQ + (round & 1) * STG;
-          if (h == 0) bulk_wait_group_read<1>();  // this buffer's previous reduce has read it
-          named_bar_sync(1, 128);
-          // row-major [32 q][128 h] fp32: a warp's 32 head dims are one 128 B row
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const uint32_t addr = buf + q * 512 + h * 4;
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v[32 * r2 + q]) : "memory");
-          }
-          fence_proxy_async_smem();
-          named_bar_sync(1, 128);
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
 #ifdef A2D_X_NO_DQ
-          if (false) {
+        if (false) {
 #else
-          if (h == 0) {
+        if (h == 0) {
 #endif
-            tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + 64 * half + 32 * r2, bh);
-            bulk_commit_group();
-          }
+          tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + 32 * r, bh);
+          bulk_commit_group();
         }
       }
     }

@@ -7,21 +7,21 @@ rm -rf /tmp/xt && mkdir -p /tmp/xt && cp $R/*.cu $R/*.cuh $R/*.h /tmp/xt/
 sed -i 's|../../include/attn2d_b200.h|/root/repo/include/attn2d_b200.h|' /tmp/xt/*
 python3 - <<'PY'
 p='/tmp/xt/tile_bwd128.cu'; s=open(p).read()
-ev = [("mbar_wait(bar(B_QEMPTY0 + qs), ((i >> 1) & 1) ^ 1);", 0, 0, 'after'),
-      ("tma_load_3d(sb + OFF_DO + s * SLAB, &tm_do, bar(B_DOFULL), s * 64, qrow, bh);", 1, 0, 'after'),
+ev = [("const int qrow0 = cur.row0(p.q_map);", 0, 4, 'after'),
+      ("mbar_wait(bar(B_QFULL0 + qs), (i >> 1) & 1);", 1, 4, 'before'),
       ("mbar_wait(bar(B_DOFULL), i & 1);", 2, 1, 'after'),
       ("mbar_wait(bar(B_PREADY), i & 1);", 3, 1, 'after'),
       ("mbar_wait(bar(B_DSREADY), i & 1);", 4, 1, 'after'),
       ("mbar_wait(bar(B_QFULL0 + (qs ^ 1)), ((i + 1) >> 1) & 1);", 5, 1, 'after'),
       ("mbar_wait(bar(B_DQFREE), (i - 1) & 1);", 6, 1, 'after'),
-      ("mbar_wait(bar(B_QFULL0 + qs), (i >> 1) & 1);", 7, 2, 'after'),
-      ("mbar_wait(bar(B_SFULL), i & 1);", 8, 2, 'after'),
-      ("mbar_arrive(bar(B_PREADY));", 9, 2, 'before'),
-      ("mbar_wait(bar(B_DPFULL), i & 1);", 10, 2, 'after'),
-      ("if (i > 0) mbar_wait(bar(B_DSFREE), (i - 1) & 1);", 11, 2, 'after'),
-      ("mbar_arrive(bar(B_DSREADY));", 12, 2, 'before'),
-      ("mbar_wait(bar(B_DQFULL), i & 1);", 13, 10, 'after'),
-      ("mbar_arrive(bar(B_DQFREE));", 14, 10, 'before'),
+      ("mbar_wait(bar(B_QFULL0 + qs), (i >> 1) & 1);", 7, 4, 'after'),
+      ("mbar_wait(bar(B_SFULL), i & 1);", 8, 4, 'after'),
+      ("mbar_arrive(bar(B_PREADY));", 9, 4, 'before'),
+      ("mbar_wait(bar(B_DPFULL), i & 1);", 10, 4, 'after'),
+      ("if (i > 0) mbar_wait(bar(B_DSFREE), (i - 1) & 1);", 11, 4, 'after'),
+      ("mbar_arrive(bar(B_DSREADY));", 12, 4, 'before'),
+      ("mbar_wait(bar(B_DQFULL), i & 1);", 13, 12, 'after'),
+      ("mbar_arrive(bar(B_DQFREE));", 14, 12, 'before'),
       ("bulk_commit_group();", 15, 12, 'after')]
 for pat, e, w, where in ev:
     assert pat in s, pat

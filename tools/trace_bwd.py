@@ -23,7 +23,7 @@ torch.cuda.synchronize()
 buf = np.zeros((16, 1024), dtype=np.int64)
 lib = _lib.load()
 lib.a2d_trace_dump(ctypes.c_void_p(buf.ctypes.data))
-names = ["P:qempty", "P:do_issued", "M:dofull", "M:pready", "M:dsready", "M:qfull+1", "M:dqfree",
+names = ["S:looptop", "S:preqfull", "M:dofull", "M:pready", "M:dsready", "M:qfull+1", "M:dqfree",
          "S:qfull", "S:sfull", "S:P_arrive", "S:dpfull", "S:dsfree", "S:DS_arrive", "D:dqfull",
          "D:dqfree_arr", "D:last_commit"]
 t0 = buf[buf > 0].min()
