@@ -13,6 +13,8 @@ int check_launch(const char* what);
 
 int launch_tile_fwd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, cudaStream_t stream);
+int launch_tile_fwd2(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                     const CUtensorMap& tv, cudaStream_t stream);
 int launch_tile_bwd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream);
 int launch_lse_merge(const float* o_parts, const float* lse_parts, int k_parts,
