@@ -17,6 +17,17 @@ A2D_DEV uint32_t smem_u32(const void* p) {
 
 A2D_DEV uint32_t lane_id() { return threadIdx.x & 31; }
 
+// One elected lane of a converged warp (elect.sync): lets a whole warp run
+// a single-thread role (MMA issue) with warp-uniform control flow, so the
+// compiler keeps descriptors in uniform registers.
+A2D_DEV bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---------------------------------------------------------------- mbarrier
 A2D_DEV void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -44,6 +55,25 @@ A2D_DEV uint32_t mbar_try_wait(uint32_t bar, uint32_t parity) {
 }
 A2D_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// try_wait with a suspend-time hint: the waiting thread is parked by the
+// hardware until the phase completes (or the hint expires) instead of
+// spinning, so single-thread roles (TMA producer, MMA issuer) stop stealing
+// issue slots from the math warps sharing their SM sub-partition.
+A2D_DEV uint32_t mbar_try_wait_hint(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(0x100000)
+      : "memory");
+  return ok;
+}
+A2D_DEV void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait_hint(bar, parity)) {
   }
 }
 
@@ -244,6 +274,22 @@ A2D_DEV float2 exp2_poly2(float2 x) {
   const int ex = (__float_as_int(t.x) << 23) + __float_as_int(p.x);
   const int ey = (__float_as_int(t.y) << 23) + __float_as_int(p.y);
   return make_float2(__int_as_float(ex), __int_as_float(ey));
+}
+// max over N (64 or 128) values: 8 independent FMNMX3 chains, then a tree
+template <int N>
+A2D_DEV float rowmax(const float* s) {
+  float m[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = fmaxf(s[i], s[8 + i]);
+#pragma unroll
+  for (int k = 16; k < N; k += 16) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = fmax3(m[i], s[k + i], s[k + 8 + i]);
+  }
+  const float a = fmax3(m[0], m[1], m[2]);
+  const float b = fmax3(m[3], m[4], m[5]);
+  const float c = fmaxf(m[6], m[7]);
+  return fmax3(a, b, c);
 }
 // max over 128 values: 8 independent FMNMX3 chains, then a 3-level tree
 A2D_DEV float rowmax128(const float* s) {

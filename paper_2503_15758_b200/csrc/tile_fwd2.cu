@@ -7,12 +7,17 @@
 // for one softmax warpgroup: each CTA owns TWO 128-row query tiles of one
 // head and sweeps their common key range once.
 //
-// Warp roles (320 threads = 200 registers each, one CTA per SM):
+// Warp roles (one CTA per SM; CS = column split of the softmax, 1 or 2):
 //   warp 0       TMA producer: Q0/Q1 once, then K (3-stage) / V (2-stage) rings
-//   warp 1       tcgen05 MMA issuer (one elected lane) + TMEM owner
-//   warps 2-5    softmax warpgroup 0 (query tile 0, one row per thread; warp w
-//                owns TMEM lanes 32*(w%4)..+31)
-//   warps 6-9    softmax warpgroup 1 (query tile 1)
+//   warp 1       tcgen05 MMA issuer (whole warp, one elected lane issues)
+//   warps 2-3    idle (complete the register-reallocation warpgroup)
+//   warps 4..    2*CS softmax warpgroups: warpgroup (t, h) owns query tile t,
+//                key columns [h*128/CS, (h+1)*128/CS) of every S tile; warp w
+//                owns TMEM lanes 32*(w%4)..+31 (one query row per thread).
+//                With CS = 2 the two halves of a row exchange their maxima
+//                through shared memory (64-thread named barrier per row
+//                quarter), halving the per-tile softmax latency that sits on
+//                the S -> P -> PV -> S critical path.
 // TMEM (512 columns): S0 [0,128), S1 [128,256), O0 [256,256+H), O1 after it.
 // P_t overwrites the first 64 columns of S_t and is the TMEM A operand of
 // O_t += P_t V.  Per key tile j the MMA order is
@@ -27,11 +32,45 @@
 #include "tiles.cuh"
 #include "kernels.h"
 
+// which exponential pairs go to the FMA-pipe polynomial (MUFU offload)
+#if defined(F2X_ALLMUFU)
+#define F2_POLY(jj) false
+#elif defined(F2X_POLYHALF)
+#define F2_POLY(jj) (((jj) >> 1) & 1)
+#elif defined(F2X_POLY3)
+#define F2_POLY(jj) ((((jj) >> 1) & 7) == 1 || (((jj) >> 1) & 7) == 4 || (((jj) >> 1) & 7) == 6)
+#else
+#define F2_POLY(jj) ((((jj) >> 1) & 3) == 3)
+#endif
+#ifdef F2X_NOEXP
+#define XEX2(x) (x)
+#else
+#define XEX2(x) ex2(x)
+#endif
+#ifdef F2X_SPIN
+#define F2_WAIT mbar_wait
+#else
+#define F2_WAIT mbar_wait_sleep
+#endif
+
+#ifdef F2X_TRACE
+__device__ long long g_f2trace[48][1024];
+extern "C" int a2d_trace_dump(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_f2trace, sizeof(g_f2trace));
+}
+#define TR(row, i)                                                                  \
+  do {                                                                              \
+    if (blockIdx.x == TX && blockIdx.y == TY && (threadIdx.x & 31) == 0 && (i) < 1024) \
+      g_f2trace[row][i] = clock64();                                                \
+  } while (0)
+#else
+#define TR(row, i) ((void)0)
+#endif
+
 namespace a2d {
 
 namespace {
 
-constexpr int F2_THREADS = 384;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;
@@ -57,16 +96,17 @@ struct F2Layout {
   static constexpr int B_ODONE = B_PFULL + 2;     // [2]: last PV_t done
   static constexpr int NBAR = B_ODONE + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
-  static constexpr int SMEM = OFF_TMEMPTR + 16;
+  static constexpr int OFF_XCH = OFF_TMEMPTR + 16;  // [2 tiles][2 halves][128 rows] fp32
+  static constexpr int SMEM = OFF_XCH + 2 * 2 * 128 * 4;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 constexpr uint32_t TMEM_COLS = 512;
 
-template <int HD>
+template <int HD, int NCOL>
 __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t tmem_o,
                                             bool have_o, int bh, int grow, bool valid,
-                                            float m_run, float l_run) {
+                                            float m_run, float l_run, int col0, bool write_lse) {
   const float lse_new = (l_run > 0.f) ? (m_run + lg2(l_run)) * kLn2 : -INFINITY;
   float w_new = (l_run > 0.f) ? 1.f / l_run : 0.f;
   float w_old = 0.f;
@@ -88,9 +128,9 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
       lse_out = mxl + __logf(eo + en);
     }
   }
-  if (valid) *lse_ptr = lse_out;
+  if (valid && write_lse) *lse_ptr = lse_out;
 #pragma unroll
-  for (int c = 0; c < HD / 32; ++c) {
+  for (int c = 0; c < NCOL / 32; ++c) {
     float o[32];
     if (have_o) {
       tmem_ld32(tmem_o + c * 32, o);
@@ -102,7 +142,7 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
     if (!valid) continue;
     if (p.o_dtype == A2D_F32) {
       float* dst = reinterpret_cast<float*>(p.o) + (long long)bh * p.o_stride_bh +
-                   (long long)grow * p.o_stride_row + c * 32;
+                   (long long)grow * p.o_stride_row + col0 + c * 32;
       if (p.accumulate) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
@@ -122,7 +162,7 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
       }
     } else {
       __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + (long long)bh * p.o_stride_bh +
-                           (long long)grow * p.o_stride_row + c * 32;
+                           (long long)grow * p.o_stride_row + col0 + c * 32;
 #pragma unroll
       for (int i = 0; i < 32; i += 8) {
         uint4 v;
@@ -136,8 +176,13 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
   }
 }
 
-template <int HD>
-__global__ void __launch_bounds__(F2_THREADS, 1)
+template <int CS>
+struct F2Threads {
+  static constexpr int N = 128 + 256 * CS;
+};
+
+template <int HD, int CS>
+__global__ void __launch_bounds__(F2Threads<CS>::N, 1)
     fwd2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ a2d_tile_fwd_args p,
                 int q_tiles) {
@@ -166,7 +211,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(bar(L::B_SFULL + t), 1);
-      mbar_init(bar(L::B_PFULL + t), 128);
+      mbar_init(bar(L::B_PFULL + t), 128 * CS);
       mbar_init(bar(L::B_ODONE + t), 1);
     }
     fence_mbar_init();
@@ -197,7 +242,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   const int rot = pair;  // rotated key sweep
 
   if (warp < 4) {
-    regs_dec<96>();
+    if constexpr (CS == 1) regs_dec<96>(); else regs_dec<32>();
     if (warp == 0 && lane == 0 && n_tiles > 0) {
       // -------------------------------------------------------- producer
       mbar_expect_tx(bar(L::B_Q), 2 * L::TILE_BYTES);
@@ -212,145 +257,232 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       int ks = 0, kph = 0, vs = 0, vph = 0;
       for (int j = 0; j < n_tiles; ++j, cur.next(kr)) {
         const int krow = cur.row0(p.k_map);
-        mbar_wait(bar(L::B_KEMPTY + ks), kph ^ 1);
+        F2_WAIT(bar(L::B_KEMPTY + ks), kph ^ 1);
+        TR(45, j);
+#ifdef F2X_NOTMA
+        if (j >= L::KST) {
+          mbar_arrive(bar(L::B_KFULL + ks));
+          if (++ks == L::KST) { ks = 0; kph ^= 1; }
+          F2_WAIT(bar(L::B_VEMPTY + vs), vph ^ 1);
+          mbar_arrive(bar(L::B_VFULL + vs));
+          if (++vs == L::VST) { vs = 0; vph ^= 1; }
+          continue;
+        }
+#endif
         mbar_expect_tx(bar(L::B_KFULL + ks), L::TILE_BYTES);
         for (int s = 0; s < L::SLABS; ++s)
           tma_load_3d(sb + L::OFF_K + ks * L::TILE_BYTES + s * L::SLAB, &tm_k,
                       bar(L::B_KFULL + ks), s * 64, krow, bh);
         if (++ks == L::KST) { ks = 0; kph ^= 1; }
-        mbar_wait(bar(L::B_VEMPTY + vs), vph ^ 1);
+        F2_WAIT(bar(L::B_VEMPTY + vs), vph ^ 1);
+        TR(46, j);
         mbar_expect_tx(bar(L::B_VFULL + vs), L::TILE_BYTES);
         for (int s = 0; s < L::SLABS; ++s)
           tma_load_3d(sb + L::OFF_V + vs * L::TILE_BYTES + s * L::SLAB, &tm_v,
                       bar(L::B_VFULL + vs), s * 64, krow, bh);
         if (++vs == L::VST) { vs = 0; vph ^= 1; }
       }
-    } else if (warp == 1 && lane == 0 && n_tiles > 0) {
-      // -------------------------------------------------------- MMA issuer
+    } else if (warp == 1 && n_tiles > 0) {
+      // -------------------------------------------------------- MMA issuer (whole warp, one elected lane issues)
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, HD, 0, 1);
       int ks = 0, kph = 0, vs = 0, vph = 0;
-      mbar_wait(bar(L::B_Q), 0);
+      F2_WAIT(bar(L::B_Q), 0);
+      // Descriptors are built once; per MMA only a constant is added to the
+      // start-address field (16-byte units, no carry: shared memory < 256 KB),
+      // so the issue loop keeps pace with the 64-cycle N=128 MMA even while
+      // two softmax warps share this warp's sub-partition.
+      const uint64_t dq0 = make_sdesc(sb + L::OFF_Q, 16, 1024);
+      const uint64_t dk0 = make_sdesc(sb + L::OFF_K, 16, 1024);
+      const uint64_t dv0 = make_sdesc(sb + L::OFF_V, L::SLAB, 1024);
       auto issue_qk = [&](int t) {  // S_t = Q_t K^T on the current K stage
-        const uint32_t qbase = sb + L::OFF_Q + t * L::TILE_BYTES;
-        const uint32_t kbase = sb + L::OFF_K + ks * L::TILE_BYTES;
+        const uint64_t dq = dq0 + uint64_t(t * (L::TILE_BYTES >> 4));
+        const uint64_t dk = dk0 + uint64_t(ks * (L::TILE_BYTES >> 4));
+        const uint32_t d = tmem + t * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * L::SLAB + (kk & 3) * 32;
-          umma_bf16(tmem + t * 128, make_sdesc(qbase + off, 16, 1024),
-                    make_sdesc(kbase + off, 16, 1024), idesc_qk, kk > 0);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint64_t off = uint64_t(((kk >> 2) * L::SLAB + (kk & 3) * 32) >> 4);
+            umma_bf16(d, dq + off, dk + off, idesc_qk, kk > 0);
+          }
+          umma_commit(bar(L::B_SFULL + t));
         }
-        umma_commit(bar(L::B_SFULL + t));
+        __syncwarp();
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P_t V on the current V stage
-        const uint32_t vbase = sb + L::OFF_V + vs * L::TILE_BYTES;
+        const uint64_t dv = dv0 + uint64_t(vs * (L::TILE_BYTES >> 4));
         const uint32_t pcol = tmem + t * 128;
         const uint32_t ocol = tmem + (t ? TM_O1 : TM_O0);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk)
-          umma_bf16_ts(ocol, pcol + kk * 8, make_sdesc(vbase + kk * 2048, L::SLAB, 1024),
-                       idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < TILE / 16; ++kk)
+            umma_bf16_ts(ocol, pcol + kk * 8, dv + uint64_t(kk * (2048 >> 4)), idesc_pv,
+                         (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        __syncwarp();
+      };
+      auto commit = [&](int b) {
+        if (elect_one()) umma_commit(bar(b));
+        __syncwarp();
       };
       // prologue: S0(0), S1(0)
-      mbar_wait(bar(L::B_KFULL + ks), kph);
+      F2_WAIT(bar(L::B_KFULL + ks), kph);
       tc_fence_after();
       issue_qk(0);
       issue_qk(1);
-      umma_commit(bar(L::B_KEMPTY + ks));
+      commit(L::B_KEMPTY + ks);
       if (++ks == L::KST) { ks = 0; kph ^= 1; }
       for (int j = 0; j < n_tiles; ++j) {
         const bool more = j + 1 < n_tiles;
-        mbar_wait(bar(L::B_VFULL + vs), vph);
+        F2_WAIT(bar(L::B_VFULL + vs), vph);
+        TR(44, j);
         // ---- tile 0: PV0(j), QK0(j+1)
-        mbar_wait(bar(L::B_PFULL + 0), j & 1);
+        F2_WAIT(bar(L::B_PFULL + 0), j & 1);
         tc_fence_after();
+        TR(40, j);
         issue_pv(0, j);
         if (more) {
-          mbar_wait(bar(L::B_KFULL + ks), kph);
+          F2_WAIT(bar(L::B_KFULL + ks), kph);
           tc_fence_after();
           issue_qk(0);
+          TR(41, j);
         } else {
-          umma_commit(bar(L::B_ODONE + 0));
+          commit(L::B_ODONE + 0);
         }
         // ---- tile 1: PV1(j), QK1(j+1)
-        mbar_wait(bar(L::B_PFULL + 1), j & 1);
+        F2_WAIT(bar(L::B_PFULL + 1), j & 1);
         tc_fence_after();
+        TR(42, j);
         issue_pv(1, j);
-        umma_commit(bar(L::B_VEMPTY + vs));
+        commit(L::B_VEMPTY + vs);
         if (++vs == L::VST) { vs = 0; vph ^= 1; }
         if (more) {
           issue_qk(1);
-          umma_commit(bar(L::B_KEMPTY + ks));
+          TR(43, j);
+          commit(L::B_KEMPTY + ks);
           if (++ks == L::KST) { ks = 0; kph ^= 1; }
         } else {
-          umma_commit(bar(L::B_ODONE + 1));
+          commit(L::B_ODONE + 1);
         }
       }
     }
   } else {
-    regs_inc<200>();
+    if constexpr (CS == 1) regs_inc<200>(); else regs_inc<112>();
     // ------------------------------------------------------------ softmax WGs
-    const int t = (warp - 4) >> 2;  // query tile of this warpgroup
+    constexpr int NC = TILE / CS;  // key columns of S per thread
+    const int sidx = warp - 4;
+    const int t = sidx / (4 * CS);  // query tile of this warpgroup
+    const int h = (sidx >> 2) % CS;  // column half
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr + t * 128;
-    const uint32_t o_addr = tmem + lane_addr + (t ? TM_O1 : TM_O0);
+    const uint32_t s_addr = tmem + lane_addr + t * 128 + h * NC;
+    const uint32_t p_addr = tmem + lane_addr + t * 128 + h * (NC / 2);
+    const uint32_t o_addr = tmem + lane_addr + (t ? TM_O1 : TM_O0) + h * (HD / CS);
+    float* xch = reinterpret_cast<float*>(smem + L::OFF_XCH) + t * 256;
+    const uint32_t xbar = 1 + t * 4 + quarter;  // named barrier of this row quarter's halves
     const bool present = (t == 0) || has1;
     const TileRef qt = t ? qt1 : qt0;
     const float sl2 = p.scale * kLog2e;
-    float m_run = -INFINITY;  // running max of scale*log2e*s
-    float l_run = 0.f;
+    float m_run = -INFINITY;  // running max of scale*log2e*s (common to both halves)
+    float l_run = 0.f;        // this half's share of the denominator
+    // Per-tile mask classes for affine maps are computed 32 tiles at a time,
+    // one tile per lane, and broadcast with one shuffle per tile: the sweep
+    // itself carries no index arithmetic.  Explicit index arrays keep the
+    // per-tile binary-search path.
+    const bool arr = p.q_map.mode == A2D_IDX_ARRAY;
+    const int rot0 = n_tiles > 0 ? rot % n_tiles : 0;
+    uint32_t my_info = 0;
     TileCursor cur;
-    cur.start(kr, rot);
-    for (int j = 0; j < n_tiles; ++j, cur.next(kr)) {
-      const TileRef kt = tile_ref(p.k_map, p.nk, cur.row0(p.k_map));
-      PairMask pm;
-      int lim = TILE - 1;
-      if (present) {
-        pm = pair_mask(p.q_map, qt, kt, causal);
-        if (pm.partial) lim = row_limit(p.q_map, p.k_map, qt, kt, pm, causal, row);
-      } else {
-        pm.partial = true;
+    if (arr) cur.start(kr, rot);
+    for (int j = 0; j < n_tiles; ++j) {
+      bool partial;
+      int lim = TILE - 1;  // last visible key column of this row (tile-relative)
+      if (!present) {
+        partial = true;
         lim = -1;
+      } else if (arr) {
+        const TileRef kt = tile_ref(p.k_map, p.nk, cur.row0(p.k_map));
+        cur.next(kr);
+        const PairMask pm = pair_mask(p.q_map, qt, kt, causal);
+        partial = pm.partial;
+        if (partial) lim = row_limit(p.q_map, p.k_map, qt, kt, pm, causal, row);
+      } else {
+        if ((j & 31) == 0) {
+          const int f = j + lane;
+          my_info = 0;
+          if (f < n_tiles) {
+            const int g = rot0 + f < n_tiles ? rot0 + f : rot0 + f - n_tiles;
+            const TileRef kt = tile_ref(p.k_map, p.nk, range_row0(kr, p.k_map, g));
+            const PairMask q = pair_mask(p.q_map, qt, kt, causal);
+            my_info = uint32_t(q.thr + 512) | (uint32_t(q.kvalid) << 16) |
+                      (q.partial ? 0x80000000u : 0u);
+          }
+        }
+        const uint32_t inf = __shfl_sync(0xffffffffu, my_info, j & 31);
+        partial = (inf >> 31) != 0;
+        if (partial) {
+          const int kvalid = int((inf >> 16) & 0xff);
+          lim = causal ? min(row - (int(inf & 0xffff) - 512), kvalid - 1) : kvalid - 1;
+        }
       }
+      lim -= h * NC;  // relative to this half's first column
       mbar_wait(bar(L::B_SFULL + t), j & 1);
       tc_fence_after();
-      float s[TILE];
+      TR(0 * 8 + t * 4 + quarter, j);
+#ifdef F2X_NOSOFTMAX
+      if (true) {
+        tc_fence_before();
+        mbar_arrive(bar(L::B_PFULL + t));
+        continue;
+      }
+#endif
+      float s[NC];
 #pragma unroll
-      for (int c = 0; c < TILE / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
+      for (int c = 0; c < NC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
       tmem_wait_ld();
-      if (pm.partial) {
+      TR(1 * 8 + t * 4 + quarter, j);
+      if (partial) {
 #pragma unroll
-        for (int jj = 0; jj < TILE; ++jj)
+        for (int jj = 0; jj < NC; ++jj)
           if (jj > lim) s[jj] = -INFINITY;
       }
-      const float mx = rowmax128(s);
-      const float m_new = fmaxf(m_run, mx * sl2);
+      float mx = rowmax<NC>(s) * sl2;
+      if constexpr (CS == 2) {
+        // both halves of a row need one common max: exchange through smem.
+        // One slot per (tile, half, row) suffices: the partner reads it
+        // before arriving on PFULL(j), and this slot is rewritten only after
+        // S(j+1), i.e. after PV(j) consumed both halves' P.
+        xch[h * 128 + row] = mx;
+        named_bar_sync(xbar, 64);
+        mx = fmaxf(mx, xch[(h ^ 1) * 128 + row]);
+      }
+      const float m_new = fmaxf(m_run, mx);
       float alpha = 1.f;
       if (m_new > m_run + kRescaleThreshold) {
         alpha = ex2(m_run - m_new);
         m_run = m_new;
       }
       const float mb = (m_run == -INFINITY) ? 0.f : m_run;
-      uint32_t pk[TILE / 2];
+      TR(2 * 8 + t * 4 + quarter, j);
+      uint32_t pk[NC / 2];
       float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
       const float2 sc = make_float2(sl2, sl2), nb = make_float2(-mb, -mb);
-      if (pm.partial) {  // masked entries are -inf: the exact MUFU path keeps them 0
+      if (partial) {  // masked entries are -inf: the exact MUFU path keeps them 0
 #pragma unroll
-        for (int jj = 0; jj < TILE; jj += 2) {
+        for (int jj = 0; jj < NC; jj += 2) {
           const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
-          const float2 e = make_float2(ex2(x.x), ex2(x.y));
+          const float2 e = make_float2(XEX2(x.x), XEX2(x.y));
           acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
           pk[jj / 2] = pack_bf16(e.x, e.y);
         }
       } else {  // a quarter of the exponentials on the FMA pipe (MUFU offload)
 #pragma unroll
-        for (int jj = 0; jj < TILE; jj += 2) {
+        for (int jj = 0; jj < NC; jj += 2) {
           const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
           float2 e;
-          if (((jj >> 1) & 3) == 3) e = exp2_poly2(x);
-          else e = make_float2(ex2(x.x), ex2(x.y));
+          if (F2_POLY(jj)) e = exp2_poly2(x);
+          else e = make_float2(XEX2(x.x), XEX2(x.y));
           acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
           pk[jj / 2] = pack_bf16(e.x, e.y);
         }
@@ -358,14 +490,18 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
       const float2 a = fadd2(a01, a23);
       l_run = l_run * alpha + (a.x + a.y);
-      // P_t(j) over the first 64 columns of S_t (the S values were consumed above)
-      tmem_st32(s_addr, reinterpret_cast<const float*>(pk));
-      tmem_st32(s_addr + 32, reinterpret_cast<const float*>(pk + 32));
+      TR(3 * 8 + t * 4 + quarter, j);
+      // P_t(j), this half's keys, over S_t columns that are already consumed
+      // (half 1 writes columns 32..63 of S, which half 0 loaded before the
+      // exchange barrier)
+#pragma unroll
+      for (int c = 0; c < NC / 64; ++c)
+        tmem_st32(p_addr + c * 32, reinterpret_cast<const float*>(pk + c * 32));
       // O_t already holds PV_t(j-1) (its commit preceded S_t(j)'s): rescale
-      // in place when this warp's running max moved
+      // this half's columns in place when the running max moved
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = 0; c < HD / CS / 32; ++c) {
           float o[32];
           tmem_ld32(o_addr + c * 32, o);
           tmem_wait_ld();
@@ -376,6 +512,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       }
       tmem_wait_st();
       tc_fence_before();
+      TR(4 * 8 + t * 4 + quarter, j);
       mbar_arrive(bar(L::B_PFULL + t));
     }
     // ------------------------------------------------------------ epilogue
@@ -383,8 +520,14 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       mbar_wait(bar(L::B_ODONE + t), 0);
       tc_fence_after();
     }
+    if constexpr (CS == 2) {  // the row's denominator is the sum of both halves
+      xch[h * 128 + row] = l_run;
+      named_bar_sync(xbar, 64);
+      l_run += xch[(h ^ 1) * 128 + row];
+    }
     if (present)
-      f2_epilogue<HD>(p, o_addr, n_tiles > 0, bh, qt.row0 + row, row < qt.nvalid, m_run, l_run);
+      f2_epilogue<HD, HD / CS>(p, o_addr, n_tiles > 0, bh, qt.row0 + row, row < qt.nvalid, m_run,
+                               l_run, h * (HD / CS), h == 0);
   }
 
   tc_fence_before();
@@ -397,7 +540,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
 
 }  // namespace
 
-template <int HD>
+template <int HD, int CS>
 int launch_fwd2_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                    const CUtensorMap& tv, cudaStream_t stream) {
   using L = F2Layout<HD>;
@@ -405,7 +548,7 @@ int launch_fwd2_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUte
   int dev = 0;
   cudaGetDevice(&dev);
   if (!configured[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(fwd2_kernel<HD>,
+    cudaError_t e = cudaFuncSetAttribute(fwd2_kernel<HD, CS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fwd2)");
     configured[dev & 63] = true;
@@ -414,14 +557,22 @@ int launch_fwd2_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUte
                           ? a.q_map.nblocks * (a.q_map.rows_per_block / TILE)
                           : (a.nq + TILE - 1) / TILE;
   dim3 grid((q_tiles + 1) / 2, a.bh);
-  fwd2_kernel<HD><<<grid, F2_THREADS, L::SMEM, stream>>>(tq, tk, tv, a, q_tiles);
+  fwd2_kernel<HD, CS><<<grid, F2Threads<CS>::N, L::SMEM, stream>>>(tq, tk, tv, a, q_tiles);
   return check_launch("fwd2_kernel");
 }
 
 int launch_tile_fwd2(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                      const CUtensorMap& tv, cudaStream_t stream) {
-  if (a.h == 128) return launch_fwd2_hd<128>(a, tq, tk, tv, stream);
-  return launch_fwd2_hd<64>(a, tq, tk, tv, stream);
+  // CS = 2 (column-split softmax, 640 threads) measured slower on B200:
+  // the SM sub-partitions are throughput-bound, not latency-bound, so the
+  // extra warps only add the max exchange (kept for experiments: -DF2X_CS2)
+#ifdef F2X_CS2
+  constexpr int CS = 2;
+#else
+  constexpr int CS = 1;
+#endif
+  if (a.h == 128) return launch_fwd2_hd<128, CS>(a, tq, tk, tv, stream);
+  return launch_fwd2_hd<64, CS>(a, tq, tk, tv, stream);
 }
 
 }  // namespace a2d

@@ -190,6 +190,20 @@ struct TileCursor {
   }
 };
 
+// Local row0 of the tile at flat position f (0 <= f < r.total) of a
+// TileRange in block-major order (random access twin of TileCursor).
+__device__ __forceinline__ int range_row0(const TileRange& r, const a2d_index_map& m, int f,
+                                          int T = TILE) {
+  int b = 0;
+  for (; b < r.nblk - 1; ++b) {
+    const int cnt = r.last[b] - r.first[b];
+    if (f < cnt) break;
+    f -= cnt;
+  }
+  const int rpb = (m.mode == A2D_IDX_ARRAY || m.nblocks == 1) ? 0 : m.rows_per_block;
+  return b * rpb + (r.first[b] + f) * T;
+}
+
 // Causal visibility inside a (query tile, key tile) pair: query row ii
 // (0..127) sees key columns 0..lim(ii).  Returns whether any masking is
 // needed.  Affine maps share one stride s, so q_g >= k_g  <=>
@@ -213,7 +227,7 @@ __device__ __forceinline__ PairMask pair_mask(const a2d_index_map& qm, const Til
     pm.partial = true;  // per-row binary search
     return pm;
   }
-  long long thr = ceil_div_s(kt.gmin - qt.gmin, qm.stride);
+  long long thr = qm.stride == 1 ? kt.gmin - qt.gmin : ceil_div_s(kt.gmin - qt.gmin, qm.stride);
   thr = max(-(long long)TILE, min((long long)(2 * TILE), thr));
   pm.thr = (int)thr;
   pm.partial = (kt.nvalid < TILE) || (pm.thr > -(TILE - 1));
