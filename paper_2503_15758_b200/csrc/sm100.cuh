@@ -86,6 +86,9 @@ A2D_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;"
 A2D_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+A2D_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // Warpgroup register reallocation (all 4 warps of a warpgroup execute it).
 template <int N>

@@ -464,6 +464,14 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
         m_run = m_new;
       }
       const float mb = (m_run == -INFINITY) ? 0.f : m_run;
+#ifdef F2X_SEQ
+      // Experiment (-DF2X_SEQ, measured 2% slower): the two tile warpgroups
+      // take turns on the exponential phase: WG1's exp(j) follows
+      // WG0's exp(j), WG0's exp(j+1) follows WG1's exp(j).  Generations of
+      // the two named barriers cannot mix: a warp re-arrives only after the
+      // other warpgroup has passed the barrier it arrived on.
+      if (CS == 1 && (t == 1 || j > 0)) named_bar_sync(t == 0 ? 9 : 10, 256);
+#endif
       TR(2 * 8 + t * 4 + quarter, j);
       uint32_t pk[NC / 2];
       float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
@@ -490,6 +498,9 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
       const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
       const float2 a = fadd2(a01, a23);
       l_run = l_run * alpha + (a.x + a.y);
+#ifdef F2X_SEQ
+      if (CS == 1 && (t == 0 || j + 1 < n_tiles)) named_bar_arrive(t == 0 ? 10 : 9, 256);
+#endif
       TR(3 * 8 + t * 4 + quarter, j);
       // P_t(j), this half's keys, over S_t columns that are already consumed
       // (half 1 writes columns 32..63 of S, which half 0 loaded before the
