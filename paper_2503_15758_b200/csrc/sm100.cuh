@@ -17,6 +17,14 @@ A2D_DEV uint32_t smem_u32(const void* p) {
 
 A2D_DEV uint32_t lane_id() { return threadIdx.x & 31; }
 
+// Hides a value from loop-invariant hoisting: descriptor bases pass through
+// it inside MMA issue loops so the compiler derives the per-K-step operands
+// with one add each instead of keeping (and spilling) every variant live.
+A2D_DEV uint64_t opaque64(uint64_t x) {
+  asm volatile("" : "+l"(x));
+  return x;
+}
+
 // One elected lane of a converged warp (elect.sync): lets a whole warp run
 // a single-thread role (MMA issue) with warp-uniform control flow, so the
 // compiler keeps descriptors in uniform registers.

@@ -173,63 +173,93 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
-      if (lane == 0 && n_tiles > 0) {
+      // whole warp: warp-uniform control flow keeps descriptors in uniform
+      // registers; one elected lane issues (the single-lane version issued
+      // one MMA per ~70 cycles, slower than the 64-cycle N=128 MMA itself)
+      if (n_tiles > 0) {
         constexpr uint32_t id_ss = make_idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
         constexpr uint32_t id_kmn = make_idesc_bf16(128, 128, 0, 1);  // P^T dO, dS^T Q
         constexpr uint32_t id_mnmn = make_idesc_bf16(128, 128, 1, 1); // K^T dS^T
-        auto kmaj = [](uint32_t base, int kk) {
-          return make_sdesc(base + (kk >> 2) * SLAB + (kk & 3) * 32, 16, 1024);
+        // K-major SW128: +32 B per K16 step inside a slab, +SLAB per 64 columns;
+        // MN-major SW128: +2048 B per K16 step (16 rows of 128 B)
+        auto kofs = [](int kk) { return uint64_t(((kk >> 2) * SLAB + (kk & 3) * 32) >> 4); };
+        auto mofs = [](int kk) { return uint64_t((kk * 2048) >> 4); };
+        const uint64_t k_k = make_sdesc(sb + OFF_K, 16, 1024);
+        const uint64_t v_k = make_sdesc(sb + OFF_V, 16, 1024);
+        const uint64_t do_k = make_sdesc(sb + OFF_DO, 16, 1024);
+        const uint64_t ds_k = make_sdesc(sb + OFF_DS, 16, 1024);
+        const uint64_t q_k = make_sdesc(sb + OFF_Q, 16, 1024);
+        const uint64_t k_mn = make_sdesc(sb + OFF_K, SLAB, 1024);
+        const uint64_t ds_mn = make_sdesc(sb + OFF_DS, SLAB, 1024);
+        const uint64_t do_mn = make_sdesc(sb + OFF_DO, SLAB, 1024);
+        const uint64_t q_mn = make_sdesc(sb + OFF_Q, SLAB, 1024);
+        constexpr uint64_t QSTEP = TILE_B >> 4;
+        auto commit = [&](int b) {
+          if (elect_one()) umma_commit(bar(b));
+          __syncwarp();
         };
-        auto mnmaj = [](uint32_t base, int kk) { return make_sdesc(base + kk * 2048, SLAB, 1024); };
-        auto issue_s = [&](uint32_t col, uint32_t a_base, uint32_t b_base) {
+        auto issue_s = [&](uint32_t col, uint64_t a, uint64_t b) {
+          a = opaque64(a);
+          b = opaque64(b);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + col, kmaj(a_base, kk), kmaj(b_base, kk), id_ss, kk > 0);
+            for (int kk = 0; kk < 8; ++kk)
+              umma_bf16(tmem + col, a + kofs(kk), b + kofs(kk), id_ss, kk > 0);
+          }
+          __syncwarp();
         };
         mbar_wait(bar(B_KV), 0);
         mbar_wait(bar(B_QFULL0), 0);
         tc_fence_after();
-        issue_s(TM_X, sb + OFF_K, sb + OFF_Q);
-        umma_commit(bar(B_SFULL));
+        issue_s(TM_X, k_k, q_k);
+        commit(B_SFULL);
         for (int i = 0; i < n_tiles; ++i) {
           const int qs = i & 1;
-          const uint32_t sq = sb + OFF_Q + qs * TILE_B;
           // dP^T = V dO_i^T -> Y, once the drain has emptied dQ_{i-1} out of it
           mbar_wait(bar(B_DOFULL), i & 1);
           if (i > 0) mbar_wait(bar(B_DQFREE), (i - 1) & 1);
           tc_fence_after();
-          issue_s(TM_Y, sb + OFF_V, sb + OFF_DO);
-          umma_commit(bar(B_DPFULL));
+          issue_s(TM_Y, v_k, do_k);
+          commit(B_DPFULL);
           // dV += P^T dO_i (P^T in TMEM: warpgroup A's 64 queries at X+0, B's at X+64)
           mbar_wait(bar(B_PREADY), i & 1);
           tc_fence_after();
+          if (elect_one()) {
+            const uint64_t dob = opaque64(do_mn);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16_ts(tmem + TM_DV, tmem + TM_X + (kk >> 2) * 64 + (kk & 3) * 8,
-                         mnmaj(sb + OFF_DO, kk), id_kmn, (i > 0 || kk > 0));
-          umma_commit(bar(B_DOEMPTY));
+            for (int kk = 0; kk < 8; ++kk)
+              umma_bf16_ts(tmem + TM_DV, tmem + TM_X + (kk >> 2) * 64 + (kk & 3) * 8,
+                           dob + mofs(kk), id_kmn, (i > 0 || kk > 0));
+          }
+          __syncwarp();
+          commit(B_DOEMPTY);
           // S_{i+1} -> X: dV_i has read P_i out of X (in-order pipe)
           if (i + 1 < n_tiles) {
             mbar_wait(bar(B_QFULL0 + (qs ^ 1)), ((i + 1) >> 1) & 1);
             tc_fence_after();
-            issue_s(TM_X, sb + OFF_K, sb + OFF_Q + (qs ^ 1) * TILE_B);
-            umma_commit(bar(B_SFULL));
+            issue_s(TM_X, k_k, q_k + (qs ^ 1) * QSTEP);
+            commit(B_SFULL);
           }
           // dQ^T = K^T dS^T -> Y (dP_i was read out of Y before dS_i was published),
           // then dK += dS^T Q_i while the drain empties Y
           mbar_wait(bar(B_DSREADY), i & 1);
           tc_fence_after();
+          if (elect_one()) {
+            const uint64_t kb = opaque64(k_mn), dsb = opaque64(ds_mn);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_Y, mnmaj(sb + OFF_K, kk), mnmaj(sb + OFF_DS, kk), id_mnmn, kk > 0);
-          umma_commit(bar(B_DQFULL));
+            for (int kk = 0; kk < 8; ++kk)
+              umma_bf16(tmem + TM_Y, kb + mofs(kk), dsb + mofs(kk), id_mnmn, kk > 0);
+            umma_commit(bar(B_DQFULL));
+            const uint64_t dsk = opaque64(ds_k), qb = opaque64(q_mn + qs * QSTEP);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + TM_DK, kmaj(sb + OFF_DS, kk), mnmaj(sq, kk), id_kmn, (i > 0 || kk > 0));
-          umma_commit(bar(B_QEMPTY0 + qs));
-          umma_commit(bar(B_DSFREE));
+            for (int kk = 0; kk < 8; ++kk)
+              umma_bf16(tmem + TM_DK, dsk + kofs(kk), qb + mofs(kk), id_kmn, (i > 0 || kk > 0));
+            umma_commit(bar(B_QEMPTY0 + qs));
+            umma_commit(bar(B_DSFREE));
+          }
+          __syncwarp();
         }
-        umma_commit(bar(B_DONE));
+        commit(B_DONE);
       }
     }
   } else if (warp < 12) {
@@ -245,19 +275,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool affine = p.q_map.mode != A2D_IDX_ARRAY;
     // causal threshold of query block b against this key tile, ceil((kt.gmin -
     // base_b) / s): one division per block change instead of one per tile
-    int blk = -1;
-    long long dblk = 0;
+    // Per-tile causal classes (threshold, valid query columns, full flag)
+    // for affine maps are computed 32 tiles at a time, one tile per lane,
+    // and broadcast with one shuffle per tile; explicit index arrays keep a
+    // per-tile path.
+    const int rot0 = n_tiles > 0 ? kt_idx % n_tiles : 0;
+    uint32_t my_info = 0;
     TileCursor cur;
-    cur.start(qr, kt_idx);
-    for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
+    if (!affine) cur.start(qr, kt_idx);
+    for (int i = 0; i < n_tiles; ++i) {
       const int qs = i & 1;
-      const int qrow0 = cur.row0(p.q_map);
-      const int qend = (!affine || p.q_map.nblocks == 1) ? p.nq : (cur.b + 1) * p.q_map.rows_per_block;
-      const int qvalid = min(TILE, qend - qrow0);
       int first = 0;  // first visible query column of this key row
       bool full = true;
-      if (causal) {
-        if (!affine) {
+      if (!affine) {
+        const int qrow0 = cur.row0(p.q_map);
+        cur.next(qr);
+        const int qvalid = min(TILE, p.nq - qrow0);
+        if (causal) {
           const TileRef qt = tile_ref(p.q_map, p.nq, qrow0, TILE);
           PairMask pm;
           pm.partial = true;
@@ -265,19 +299,34 @@ __global__ void __launch_bounds__(THREADS, 1)
           pm.kvalid = kt.nvalid;
           first = col_first(p.q_map, p.k_map, qt, kt, pm, true, jj);
           full = false;
-        } else {
-          if (cur.b != blk) {
-            blk = cur.b;
-            dblk = ceil_div_s(kt.gmin - p.q_map.base[blk], p.q_map.stride);
-          }
-          long long thr = dblk - (long long)TILE * cur.t;
-          thr = max(-(long long)(2 * TILE), min((long long)(2 * TILE), thr));
-          first = jj + (int)thr;
-          full = thr <= -(TILE - 1);
         }
+        full = full && kt.nvalid == TILE && qvalid == TILE;
+      } else {
+        if ((i & 31) == 0) {
+          const int f = i + lane;
+          my_info = 0;
+          if (f < n_tiles) {
+            const int g = rot0 + f < n_tiles ? rot0 + f : rot0 + f - n_tiles;
+            int b, t;
+            range_pos(qr, g, b, t);
+            const int rpb = p.q_map.nblocks == 1 ? 0 : p.q_map.rows_per_block;
+            const int qrow0 = b * rpb + t * TILE;
+            const int qend = p.q_map.nblocks == 1 ? p.nq : (b + 1) * rpb;
+            const int qvalid = min(TILE, qend - qrow0);
+            long long thr = -(long long)(2 * TILE);
+            if (causal) {
+              thr = ceil_div_s(kt.gmin - p.q_map.base[b], p.q_map.stride) - (long long)TILE * t;
+              thr = max(-(long long)(2 * TILE), min((long long)(2 * TILE), thr));
+            }
+            const bool fl = thr <= -(TILE - 1) && kt.nvalid == TILE && qvalid == TILE;
+            my_info = uint32_t(thr + 512) | (uint32_t(qvalid) << 16) | (fl ? 0x80000000u : 0u);
+          }
+        }
+        const uint32_t inf = __shfl_sync(0xffffffffu, my_info, i & 31);
+        full = (inf >> 31) != 0;
+        first = causal ? jj + (int(inf & 0xffff) - 512) : 0;
       }
       if (!row_ok) first = TILE;
-      full = full && kt.nvalid == TILE && qvalid == TILE;
       const float* s_lse = stat + qs * 256 + c0;
       const float* s_del = s_lse + 128;
       mbar_wait(bar(B_QFULL0 + qs), (i >> 1) & 1);  // orders the producer's stats stores
@@ -317,11 +366,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       // dS = P (dP - delta), with P re-read from its bf16 pairs (the same
       // rounded P that fed dV)
+      float dpa[64];
+      tmem_ld32(tmem + lane_addr + TM_Y + c0, dpa);
+      tmem_ld32(tmem + lane_addr + TM_Y + c0 + 32, dpa + 32);
+      tmem_wait_ld();
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        float dp[32];
-        tmem_ld32(tmem + lane_addr + TM_Y + c0 + 32 * h, dp);
-        tmem_wait_ld();
+        const float* dp = dpa + 32 * h;
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
           const float2 d = fadd2(make_float2(dp[c], dp[c + 1]),

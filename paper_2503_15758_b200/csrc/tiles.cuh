@@ -190,6 +190,17 @@ struct TileCursor {
   }
 };
 
+// Block and tile (within the block) at flat position f (0 <= f < r.total).
+__device__ __forceinline__ void range_pos(const TileRange& r, int f, int& b, int& t) {
+  b = 0;
+  for (; b < r.nblk - 1; ++b) {
+    const int cnt = r.last[b] - r.first[b];
+    if (f < cnt) break;
+    f -= cnt;
+  }
+  t = r.first[b] + f;
+}
+
 // Local row0 of the tile at flat position f (0 <= f < r.total) of a
 // TileRange in block-major order (random access twin of TileCursor).
 __device__ __forceinline__ int range_row0(const TileRange& r, const a2d_index_map& m, int f,

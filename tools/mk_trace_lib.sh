@@ -34,5 +34,5 @@ extern "C" int a2d_trace_dump(long long* host) { return (int)cudaMemcpyFromSymbo
 ''', 1)
 open(p,'w').write(s)
 PY
-cd /tmp/xt && /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -DTX=$TX -DTY=$TY $XFLAGS -shared -o /root/repo/xlib/lib_TRACE$XSUF.so abi.cu tile_fwd.cu tile_bwd.cu tile_bwd128.cu lse_merge.cu selftest.cu -lcudart_static -lrt -ldl -lpthread
+cd /tmp/xt && /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -DTX=$TX -DTY=$TY $XFLAGS -shared -o /root/repo/xlib/lib_TRACE$XSUF.so abi.cu tile_fwd.cu tile_fwd2.cu tile_bwd.cu tile_bwd128.cu lse_merge.cu selftest.cu -lcudart_static -lrt -ldl -lpthread
 echo built
