@@ -20,7 +20,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu \
   > $OUT/${TAG}_launches_bench.log 2>&1
 if [ "${NCU_FULL:-1}" = "1" ]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_kernel -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd2_kernel -s 1 -c 1 \
     -o $OUT/${TAG}_fwd python tools/perf_tile.py fwd 32768 32 128 1 > $OUT/${TAG}_ncu_fwd.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:bwd128_kernel -s 1 -c 1 \
     -o $OUT/${TAG}_bwd python tools/perf_tile.py bwd 32768 32 128 1 > $OUT/${TAG}_ncu_bwd.log 2>&1
