@@ -1,7 +1,7 @@
 """Attention2D benchmark — the driver contract.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--strategy attn2d_no|ring]
+                    [--strategy attn2d_no|attn2d_o|ring]
 
 Workload (BASELINE.json metric): exact causal attention forward+backward at
 N = 131072 tokens, M = 32 heads, H = 128, B = 1, bf16 — one step is one
@@ -169,7 +169,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     from paper_2503_15758_b200 import _lib, functional, ops
     from paper_2503_15758_b200.layouts import Grid2D
-    from paper_2503_15758_b200.strategies import Attention2D, GridComm, RingAttention
+    from paper_2503_15758_b200.strategies import Attention2D, Attention2DO, GridComm, RingAttention
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -179,7 +179,7 @@ def run_ours(args, rank, world, local_rank):
     causal = True
     scale = H ** -0.5
     pr, pc = GRIDS.get(world, (1, world))
-    grid = Grid2D(pr, pc) if args.strategy == "attn2d_no" else Grid2D(1, world)
+    grid = Grid2D(pr, pc) if args.strategy in ("attn2d_no", "attn2d_o") else Grid2D(1, world)
     L = N // world
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
 
@@ -222,13 +222,14 @@ def run_ours(args, rank, world, local_rank):
                 kev["fwd"].append((e0, e1))
                 kev["bwd"].append((e2, e3))
             ops.bwd_finalize(dq_acc, scale, out=dq)
-        launches_per_step = 4  # tile_fwd, bwd_preprocess, tile_bwd, bwd_finalize
         dominant = "tile_bwd"
     else:
         dist.barrier()
         comm = GridComm(grid)
         if args.strategy == "ring":
             plan = RingAttention(comm, N, causal, scale)
+        elif args.strategy == "attn2d_o":
+            plan = Attention2DO(comm, N, causal, scale)
         else:
             plan = Attention2D(comm, N, causal, scale, head_chunks=args.head_chunks)
         q, k, v, do = (rnd((L, BH, H)) for _ in range(4))
@@ -236,11 +237,6 @@ def run_ours(args, rank, world, local_rank):
         def step(record=False):
             o_p, saved = plan.forward(q, k, v)
             plan.backward(saved, do)
-        if args.strategy == "ring":
-            launches_per_step = 2 * world + 2
-        else:
-            ch = min(args.head_chunks, BH)
-            launches_per_step = ch * (2 if pc > 1 else 1) + ch + 2
         dominant = "tile_bwd"
 
     def barrier():
@@ -258,11 +254,13 @@ def run_ours(args, rank, world, local_rank):
     kev["bwd"].clear()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ops.launches()
     ev0.record(stream)
     for _ in range(args.steps):
         step(record=True)
     ev1.record(stream)
     barrier()
+    our_launches = ops.launches() - launches0
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
@@ -345,7 +343,7 @@ def run_ours(args, rank, world, local_rank):
                        "flops_per_step": fl_step,
                        "l2": "every input is 1 GiB (> 126 MB L2); no flush needed"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+            "gpu_launches": our_launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
 
@@ -356,7 +354,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--strategy", choices=("attn2d_no", "ring"), default="attn2d_no")
+    ap.add_argument("--strategy", choices=("attn2d_no", "attn2d_o", "ring"), default="attn2d_no")
     ap.add_argument("--seq-len", type=int, default=131072)
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--head-chunks", type=int, default=4)

@@ -125,7 +125,16 @@ def _pair_maps(qi: TokenIndex, ki: TokenIndex, causal: bool, device):
 # helpers
 # --------------------------------------------------------------------------
 
+# kernels this module has launched (bench.py reports the count in the timed region)
+LAUNCHES = [0]
+
+
+def launches() -> int:
+    return LAUNCHES[0]
+
+
 def _stream(t: torch.Tensor) -> int:
+    LAUNCHES[0] += 1
     return torch.cuda.current_stream(t.device).cuda_stream
 
 

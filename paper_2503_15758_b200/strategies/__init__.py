@@ -10,11 +10,12 @@ Inputs and returned tensors are full (n, h) or (n, heads, h) arrays in
 global token order, as in the reference; each rank computes only its shard
 and the outputs are all-gathered back.  The rank-local entry points used by
 training code and the benchmark are `Attention2D` / `attention2d` and
-`RingAttention`.
+`Attention2DO` and `RingAttention`.
 
-"attn2d_o" (the reference's intra-head ring-overlap schedule,
-attn2d_o.py) is not built: head-chunk pipelining overlaps the NO schedule's
-collectives instead, so it raises ConfigError.
+Strategies: "attn2d_no" (attn2d_no.py: collective gathers, head-chunk
+pipelined), "attn2d_o" (attn2d_o.py: block rings overlapped with the tile
+kernels, at most two live receive buffers per stream) and "ring" (the
+same-kernel Ring Attention baseline).
 """
 
 from __future__ import annotations
@@ -27,17 +28,20 @@ from ..attention import count_unmasked
 from ..errors import ConfigError
 from ..layouts import Grid2D, ring_block_indices
 from .attn2d_no import Attention2D, Saved2D, attention2d
+from .attn2d_o import Attention2DO
 from .comm import GridComm
 from .common import DistAttnConfig, StrategyBackward, StrategyForward, assemble_rows
 from .ring import RingAttention
 
-STRATEGY_NAMES = ("ring", "attn2d_no")
+STRATEGY_NAMES = ("ring", "attn2d_no", "attn2d_o")
 _COMMS: dict = {}
 
 
 def get_strategy(name: str):
     if name == "attn2d_no":
         return Attention2D
+    if name == "attn2d_o":
+        return Attention2DO
     if name == "ring":
         return RingAttention
     raise ConfigError(f"unknown strategy {name!r}; expected one of {', '.join(STRATEGY_NAMES)}")
@@ -49,6 +53,7 @@ def _comm(grid: Grid2D) -> GridComm:
         _COMMS[key] = GridComm(grid)
     c = _COMMS[key]
     c.ledger.rows.clear()
+    c.buffer_peaks.clear()
     return c
 
 
@@ -66,7 +71,7 @@ def _as3(a, dev):
 
 
 def _grid_for(name: str, cfg: DistAttnConfig) -> Grid2D:
-    if name == "attn2d_no":
+    if name in ("attn2d_no", "attn2d_o"):
         return cfg.grid2d()
     if cfg.p > 1 and cfg.n % (2 * cfg.p):
         raise ConfigError(f"ring layout needs 2*p={2 * cfg.p} to divide n={cfg.n}")
@@ -108,7 +113,8 @@ def run_forward(name: str, cfg: DistAttnConfig, q, k, v, compute=None) -> Strate
     idx = torch.as_tensor(_owned(name, grid, cfg.n, comm.rank), device=dev)
     q_p, k_p, v_p = (_as3(x, dev)[idx].to(torch.bfloat16).contiguous() for x in (q, k, v))
     plan = (cls(comm, cfg.n, cfg.causal, cfg.scale, head_chunks=cfg.head_chunks, compute=compute)
-            if cls is Attention2D else cls(comm, cfg.n, cfg.causal, cfg.scale, compute=compute))
+            if cls in (Attention2D, Attention2DO)
+            else cls(comm, cfg.n, cfg.causal, cfg.scale, compute=compute))
     o_p, saved = plan.forward(q_p, k_p, v_p)
     o = _gather_full(name, grid, cfg.n, o_p.float())
     lse = _gather_full(name, grid, cfg.n, saved.lse)
@@ -117,11 +123,13 @@ def run_forward(name: str, cfg: DistAttnConfig, q, k, v, compute=None) -> Strate
                                                                "squeeze": squeeze},
                            ledger=comm.ledger, score_elements=_scores(name, grid, cfg.n,
                                                                       cfg.causal),
-                           lse=lse[:, 0] if squeeze else lse)
+                           lse=lse[:, 0] if squeeze else lse,
+                           buffer_peaks=dict(comm.buffer_peaks))
 
 
 def run_backward(name: str, cfg: DistAttnConfig, saved, d_out) -> StrategyBackward:
     plan = saved["plan"]
+    plan.comm.buffer_peaks.clear()
     grid = plan.comm.grid if hasattr(plan.comm, "grid") else Grid2D(1, cfg.p)
     dev = saved["state"].q.device
     idx = torch.as_tensor(_owned(name, grid, cfg.n, plan.comm.rank), device=dev)
@@ -131,9 +139,10 @@ def run_backward(name: str, cfg: DistAttnConfig, saved, d_out) -> StrategyBackwa
     if saved["squeeze"]:
         full = [t[:, 0] for t in full]
     return StrategyBackward(dq=full[0], dk=full[1], dv=full[2], ledger=plan.comm.ledger,
-                            score_elements=_scores(name, grid, cfg.n, cfg.causal))
+                            score_elements=_scores(name, grid, cfg.n, cfg.causal),
+                            buffer_peaks=dict(plan.comm.buffer_peaks))
 
 
-__all__ = ["STRATEGY_NAMES", "Attention2D", "DistAttnConfig", "GridComm", "RingAttention",
+__all__ = ["STRATEGY_NAMES", "Attention2D", "Attention2DO", "DistAttnConfig", "GridComm", "RingAttention",
            "Saved2D", "StrategyBackward", "StrategyForward", "attention2d", "get_strategy",
            "run_backward", "run_forward"]

@@ -71,6 +71,18 @@ class GridComm:
                     self.col_group = g
         self.ledger = ByteLedger()
         self.phase = "attention_fwd"
+        # live receive buffers per stream (the reference's buffer accounting,
+        # mesh.py:455-475): opened when a receive is posted, closed when the
+        # schedule releases the buffer
+        self.buffer_peaks: dict = {}
+        self._live: dict = defaultdict(int)
+
+    def buf_open(self, stream: str):
+        self._live[stream] += 1
+        self.buffer_peaks[stream] = max(self.buffer_peaks.get(stream, 0), self._live[stream])
+
+    def buf_close(self, stream: str):
+        self._live[stream] -= 1
 
     # ------------------------------------------------------------ helpers
     def _gather(self, t: torch.Tensor, group, n: int, op: str, async_op=False):
@@ -118,12 +130,18 @@ class GridComm:
         work = dist.all_to_all_single(out, t, group=self.row_group, async_op=async_op)
         return (out, work) if async_op else out
 
-    def exchange(self, sends: list[torch.Tensor], dst: int, src: int, op: str, async_op=False):
+    def exchange(self, sends: list[torch.Tensor], dst: int, src: int, op: str, async_op=False,
+                 recv_into: list[torch.Tensor] | None = None):
         """Send `sends` to world rank dst and receive same-shaped tensors from src
-        (the reference's send_recv, mesh.py:308-323)."""
+        (the reference's send_recv, mesh.py:308-323), optionally straight into
+        caller-provided (contiguous) buffers."""
         if dst == self.rank and src == self.rank:
+            if recv_into is not None:
+                for b, t in zip(recv_into, sends):
+                    b.copy_(t)
+                return (list(recv_into), None) if async_op else list(recv_into)
             return (list(sends), None) if async_op else list(sends)
-        recvs = [torch.empty_like(t) for t in sends]
+        recvs = list(recv_into) if recv_into is not None else [torch.empty_like(t) for t in sends]
         ops = [dist.P2POp(dist.isend, t.contiguous(), dst) for t in sends]
         ops += [dist.P2POp(dist.irecv, b, src) for b in recvs]
         reqs = dist.batch_isend_irecv(ops)

@@ -144,7 +144,7 @@ def merge_cases():
 
 def strategy_cases():
     out = {}
-    for name in ("attn2d_no", "ring"):
+    for name in ("attn2d_no", "attn2d_o", "ring"):
         for causal in (False, True):
             n, h, p = 32, 4, 4
             mask = MaskKind.CAUSAL if causal else MaskKind.NONE
@@ -159,6 +159,20 @@ def strategy_cases():
                                                    sorted(fwd.score_elements)])})
     q, k, v, d_out = gen(32, 4, seed=32 * 31 + 4)
     out.update(q=q, k=k, v=v, dout=d_out)
+    # attn2d_o receive-buffer peaks per stream on a 3x3 grid (n=36, h=4): the
+    # reference's double-buffering discipline (test_strategies.py:346-360)
+    cfg = DistAttnConfig(n=36, h=4, p=9, mask=MaskKind.CAUSAL)
+    q9, k9, v9, d9 = gen(36, 4, seed=36 * 31 + 9)
+    fwd = run_forward("attn2d_o", cfg, q9, k9, v9)
+    bwd = run_backward("attn2d_o", cfg, fwd.saved, d9)
+    peaks = {}
+    for src in (fwd.buffer_peaks, bwd.buffer_peaks):
+        for (_, stream), pk in src.items():
+            peaks[stream] = max(peaks.get(stream, 0), pk)
+    streams = sorted(peaks)
+    out.update(o_peaks_streams=np.array(streams), o_peaks=np.array([peaks[s] for s in streams]),
+               o9_q=q9, o9_k=k9, o9_v=v9, o9_dout=d9, o9_o=fwd.o, o9_dq=bwd.dq, o9_dk=bwd.dk,
+               o9_dv=bwd.dv)
     np.savez_compressed(OUT / "strategy_small.npz", **out)
 
 
@@ -192,9 +206,9 @@ def gpu_parity_cases():
 
 
 if __name__ == "__main__":
-    tile_cases()
-    merge_cases()
-    strategy_cases()
-    gpu_parity_cases()
+    only = sys.argv[1:]
+    for fn in (tile_cases, merge_cases, strategy_cases, gpu_parity_cases):
+        if not only or fn.__name__ in only:
+            fn()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -36,25 +36,38 @@ def _worker(rank, world, port, case, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import cpu_compute
+        compute = cpu_compute
+        if len(case) > 7 and case[7] == "gpu":
+            import gpu_bridge
+            compute = gpu_bridge
         from oracle import attn2d_oracle as orc
         from paper_2503_15758_b200.attention import MaskKind
         from paper_2503_15758_b200.strategies import DistAttnConfig, run_backward, run_forward
 
-        name, grid, n, h, heads, causal, golden = case
+        name, grid, n, h, heads, causal, golden = case[:7]
         cfg = DistAttnConfig(n=n, h=h, p=world, mask=MaskKind.CAUSAL if causal else MaskKind.NONE,
                              heads=heads, grid=grid, head_chunks=2 if heads > 1 else 1)
-        if golden:
+        if golden == "o9":
+            g = np.load(GOLD / "strategy_small.npz")
+            q, k, v, d_out = g["o9_q"], g["o9_k"], g["o9_v"], g["o9_dout"]
+        elif golden:
             g = np.load(GOLD / "strategy_small.npz")
             q, k, v, d_out = g["q"], g["k"], g["v"], g["dout"]
         else:
             rng = np.random.default_rng(n + world)
             q, k, v, d_out = (rng.uniform(-1, 1, (n, heads, h)) for _ in range(4))
-        fwd = run_forward(name, cfg, q, k, v, compute=cpu_compute)
+        fwd = run_forward(name, cfg, q, k, v, compute=compute)
         bwd = run_backward(name, cfg, fwd.saved, d_out)
         res = {"o": fwd.o.numpy(), "dq": bwd.dq.numpy(), "dk": bwd.dk.numpy(),
                "dv": bwd.dv.numpy(), "fwd_bytes": fwd.ledger.bytes_out("attention_fwd"),
                "bwd_bytes": bwd.ledger.bytes_out("attention_bwd"),
                "scores": np.array([fwd.score_elements[c] for c in sorted(fwd.score_elements)])}
+        peaks = {}
+        for src in (fwd.buffer_peaks, bwd.buffer_peaks):
+            for stream, pk in src.items():
+                peaks[stream] = max(peaks.get(stream, 0), pk)
+        res["peak_streams"] = np.array(sorted(peaks))
+        res["peaks"] = np.array([peaks[k] for k in sorted(peaks)])
         # dense oracle on the same bf16-rounded inputs
         rb = lambda a: torch.as_tensor(a).to(torch.bfloat16).double().numpy()
         qq, kk, vv, dd = (rb(x) for x in (q, k, v, d_out))
@@ -92,18 +105,44 @@ def test_attn2d_grids_match_dense(grid, causal):
         assert np.array_equal(r["o"], res[0]["o"])
 
 
+@pytest.mark.parametrize("grid", [(1, 2), (2, 1), (2, 2)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_attn2d_o_grids_match_dense(grid, causal):
+    res = _run(("attn2d_o", grid, 32, 4, 2, causal, False), grid[0] * grid[1])
+    for r in res[1:]:
+        assert np.array_equal(r["o"], res[0]["o"])
+
+
+def test_attn2d_o_3x3_matches_reference_and_buffer_discipline():
+    """3x3 grid, causal, against the reference's own attn2d_o outputs on the
+    same inputs, and the same per-stream receive-buffer peaks (at most two
+    live buffers; q, kv and qod really double-buffer)."""
+    res = _run(("attn2d_o", (3, 3), 36, 4, 1, True, "o9"), 9)
+    g = np.load(GOLD / "strategy_small.npz")
+    for key in ("o", "dq", "dk", "dv"):
+        want = g[f"o9_{key}"]
+        rel = np.linalg.norm(res[0][key] - want) / np.linalg.norm(want)
+        assert rel < 1e-2, (key, rel)
+    want = dict(zip(g["o_peaks_streams"].tolist(), g["o_peaks"].tolist()))
+    for r in res:
+        got = dict(zip(r["peak_streams"].tolist(), r["peaks"].tolist()))
+        assert max(got.values()) <= 2
+        for stream in ("q", "kv", "qod"):
+            assert got[stream] == want[stream] == 2, (stream, got, want)
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_ring_matches_dense(world):
     _run(("ring", None, 32, 4, 2, True, False), world)
 
 
-@pytest.mark.parametrize("name", ["attn2d_no", "ring"])
+@pytest.mark.parametrize("name", ["attn2d_no", "attn2d_o", "ring"])
 @pytest.mark.parametrize("causal", [False, True])
 def test_matches_reference_strategy_golden(name, causal):
     """Same inputs as the reference's run_forward/run_backward at n=32, h=4,
     p=4 (tests/golden/strategy_small.npz): outputs, gradients and the
     per-processor causal work counts agree."""
-    res = _run((name, (2, 2) if name == "attn2d_no" else None, 32, 4, 1, causal, True), 4)[0]
+    res = _run((name, None if name == "ring" else (2, 2), 32, 4, 1, causal, True), 4)[0]
     g = np.load(GOLD / "strategy_small.npz")
     tag = f"{name}_{'causal' if causal else 'none'}"
     for key in ("o", "dq", "dk", "dv"):
@@ -111,6 +150,20 @@ def test_matches_reference_strategy_golden(name, causal):
         rel = np.linalg.norm(res[key] - want) / np.linalg.norm(want)
         assert rel < 1e-2, (key, rel)
     assert np.array_equal(res["scores"], g[f"{tag}_scores"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,grid", [("attn2d_no", (2, 2)), ("attn2d_o", (2, 2)),
+                                       ("attn2d_o", (1, 2)), ("ring", None)])
+def test_strategies_on_cuda_kernels(name, grid):
+    """Four gloo ranks whose every tile / merge / preprocess / finalize call
+    runs on the sm_100a kernels (tests/gpu_bridge.py): the distributed
+    schedules' real call patterns (blocked cyclic index maps, accumulate
+    folds, strided dK/dV slices) against the dense oracle.  L = 128 rows per
+    rank so the gathered maps are valid multi-block affine maps."""
+    world = 4 if grid is None else grid[0] * grid[1]
+    n = (256 if name == "ring" else 128) * world  # ring halves of 128 rows
+    _run((name, grid, n, 64, 2, True, False, "gpu"), world)
 
 
 def test_attn2d_comm_volume_identity():
