@@ -58,6 +58,9 @@ def _comm(grid: Grid2D) -> GridComm:
 
 
 def _device():
+    # gloo moves host tensors (the CPU tests); NCCL / single process: the GPU
+    if dist.is_initialized() and dist.get_backend() == "gloo":
+        return torch.device("cpu")
     if torch.cuda.is_available():
         return torch.device("cuda", torch.cuda.current_device())
     return torch.device("cpu")
