@@ -299,30 +299,59 @@ def run_ours(args, rank, world, local_rank):
             t.uniform_(-1, 1)
         res = torch.empty((1,), dtype=torch.float32).pin_memory()
 
-        def e2e_step():
-            qd, kd, vd, dod = (t.to(dev, non_blocking=True) for t in hosts)
-            qd.requires_grad_(True)
-            kd.requires_grad_(True)
-            vd.requires_grad_(True)
+        # Inputs of step i+1 are copied (pinned host -> HBM, copy stream) while
+        # step i computes — a double-buffered input prefetcher, as a training
+        # loop's data pipeline would run it; every step's copies and its loss
+        # read-back stay inside the timed region.
+        cs = torch.cuda.Stream(device=dev)
+        bufs = [[torch.empty((B, M, N, H), dtype=torch.bfloat16, device=dev) for _ in range(4)]
+                for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+
+        def h2d(i):
+            s_ = i % 2
+            with torch.cuda.stream(cs):
+                if i >= 2:
+                    cs.wait_event(done[s_])  # step i-2 has finished with these buffers
+                for d_, h_ in zip(bufs[s_], hosts):
+                    d_.copy_(h_, non_blocking=True)
+                ready[s_].record(cs)
+
+        def e2e_step(i, prefetch):
+            s_ = i % 2
+            stream.wait_event(ready[s_])
+            if prefetch:
+                h2d(i + 1)
+            qd, kd, vd = (t.detach().requires_grad_(True) for t in bufs[s_][:3])
+            dod = bufs[s_][3]
             out = functional.attention(qd, kd, vd, causal=True, scale=scale)
             out.backward(dod)
             loss = (out.float() * dod.float()).sum(dtype=torch.float32)
             res.copy_(loss.reshape(1), non_blocking=True)
-        for _ in range(2):
-            e2e_step()
+            done[s_].record(stream)
+
+        def run_steps(k):
+            cs.wait_stream(stream)
+            h2d(0)
+            for i in range(k):
+                e2e_step(i, i + 1 < k)
+
+        run_steps(2)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        run_steps(args.steps)
         b.record(stream)
         torch.cuda.synchronize()
         ems = a.elapsed_time(b) / args.steps
         e2e = {"value": fl_step / (ems / 1e3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in hosts),
                "d2h_bytes_per_step": 4, "ms_per_step": ems,
-               "path": "paper_2503_15758_b200.functional.attention (autograd) with pinned host "
-                       "q/k/v/dO copied in and the loss scalar read back each step"}
+               "path": "paper_2503_15758_b200.functional.attention (autograd); pinned host "
+                       "q/k/v/dO copied to HBM every step on a copy stream (step i+1's "
+                       "copy overlaps step i's compute) and the loss scalar read back"}
+        del bufs
         del hosts
 
     cpu = None
