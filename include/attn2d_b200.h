@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define A2D_ABI_VERSION 1
+#define A2D_ABI_VERSION 2
 #define A2D_MAX_BLOCKS 16
 
 enum { A2D_OK = 0, A2D_EINVAL = 1, A2D_EUNSUPPORTED = 2, A2D_ECUDA = 3 };
@@ -73,7 +73,10 @@ typedef struct {
  *   lse [bh, nq] fp32 natural-log LSE (-inf: row attended nothing here).
  *   accumulate = 1 continues from the (o, lse) state already in the buffers
  *   (requires A2D_F32): the streaming continuation of the reference kernel
- *   (kernels/__init__.py:73-77, test_kernels.py:124-137). */
+ *   (kernels/__init__.py:73-77, test_kernels.py:124-137).
+ *   kv_group (GQA / MQA): query head b reads k/v head
+ *   b / kv_group; k/v hold bh / kv_group heads.  0 or 1 = one k/v head per
+ *   query head. */
 typedef struct {
   const void* q;
   const void* k;
@@ -91,6 +94,8 @@ typedef struct {
   int32_t accumulate;
   a2d_index_map q_map;
   a2d_index_map k_map;
+  int32_t kv_group;
+  int32_t reserved2;
 } a2d_tile_fwd_args;
 
 int a2d_tile_fwd(const a2d_tile_fwd_args* args, void* stream);
@@ -110,7 +115,9 @@ int a2d_bwd_preprocess(const void* o, const void* dout, float* delta,
  *   dq_acc [bh, nq, h] fp32 (strides dq_stride_*, multiples of 4 elements):
  *   dS K (unscaled) is ADDED to it with TMA reduce-add (caller zeroes);
  *   dk, dv [bh, nk, h]: written (dkv_dtype A2D_F32 or A2D_BF16); dk is
- *   already multiplied by scale. */
+ *   already multiplied by scale.
+ *   kv_group: as for a2d_tile_fwd (k/v hold bh / kv_group heads); dk / dv
+ *   stay per QUERY head, the caller sums each group. */
 typedef struct {
   const void* q;
   const void* k;
@@ -134,6 +141,8 @@ typedef struct {
   int32_t reserved;
   a2d_index_map q_map;
   a2d_index_map k_map;
+  int32_t kv_group;
+  int32_t reserved2;
 } a2d_tile_bwd_args;
 
 int a2d_tile_bwd(const a2d_tile_bwd_args* args, void* stream);

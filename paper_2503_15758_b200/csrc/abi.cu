@@ -176,6 +176,8 @@ int a2d_tile_fwd(const a2d_tile_fwd_args* a, void* stream) {
   if (!a) return set_error(A2D_EINVAL, "args is null");
   int rc = check_common(a->bh, a->nq, a->nk, a->h, a->causal, a->scale, a->q_map, a->k_map);
   if (rc) return rc;
+  const int g = a->kv_group > 1 ? a->kv_group : 1;
+  if (a->kv_group < 0 || a->bh % g) return set_error(A2D_EINVAL, "kv_group %d must divide bh %d", a->kv_group, a->bh);
   if (a->o_dtype != A2D_F32 && a->o_dtype != A2D_BF16)
     return set_error(A2D_EINVAL, "o_dtype invalid");
   if (a->accumulate && a->o_dtype != A2D_F32)
@@ -190,8 +192,8 @@ int a2d_tile_fwd(const a2d_tile_fwd_args* a, void* stream) {
     return set_error(A2D_EINVAL, "o strides must be multiples of 4 elements");
   CUtensorMap tq, tk, tv;
   if ((rc = make_map(&tq, a->q, a->h, a->nq, a->bh, a->q_stride_row, a->q_stride_bh, "q"))) return rc;
-  if ((rc = make_map(&tk, a->k, a->h, a->nk, a->bh, a->k_stride_row, a->k_stride_bh, "k"))) return rc;
-  if ((rc = make_map(&tv, a->v, a->h, a->nk, a->bh, a->v_stride_row, a->v_stride_bh, "v"))) return rc;
+  if ((rc = make_map(&tk, a->k, a->h, a->nk, a->bh / g, a->k_stride_row, a->k_stride_bh, "k"))) return rc;
+  if ((rc = make_map(&tv, a->v, a->h, a->nk, a->bh / g, a->v_stride_row, a->v_stride_bh, "v"))) return rc;
   return launch_tile_fwd(*a, tq, tk, tv, static_cast<cudaStream_t>(stream));
 }
 
@@ -208,6 +210,8 @@ int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
   if (!a) return set_error(A2D_EINVAL, "args is null");
   int rc = check_common(a->bh, a->nq, a->nk, a->h, a->causal, a->scale, a->q_map, a->k_map);
   if (rc) return rc;
+  const int g = a->kv_group > 1 ? a->kv_group : 1;
+  if (a->kv_group < 0 || a->bh % g) return set_error(A2D_EINVAL, "kv_group %d must divide bh %d", a->kv_group, a->bh);
   if (a->dkv_dtype != A2D_F32 && a->dkv_dtype != A2D_BF16)
     return set_error(A2D_EINVAL, "dkv_dtype invalid");
   if (!a->lse || !a->delta || !a->dq_acc || !a->dk || !a->dv)
@@ -216,8 +220,8 @@ int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
   CUtensorMap tq, tk, tv, tdo;
   const int qt = bwd_q_tile_rows(a->h);
   if ((rc = make_map(&tq, a->q, a->h, a->nq, a->bh, a->q_stride_row, a->q_stride_bh, "q", qt))) return rc;
-  if ((rc = make_map(&tk, a->k, a->h, a->nk, a->bh, a->k_stride_row, a->k_stride_bh, "k"))) return rc;
-  if ((rc = make_map(&tv, a->v, a->h, a->nk, a->bh, a->v_stride_row, a->v_stride_bh, "v"))) return rc;
+  if ((rc = make_map(&tk, a->k, a->h, a->nk, a->bh / g, a->k_stride_row, a->k_stride_bh, "k"))) return rc;
+  if ((rc = make_map(&tv, a->v, a->h, a->nk, a->bh / g, a->v_stride_row, a->v_stride_bh, "v"))) return rc;
   if ((rc = make_map(&tdo, a->dout, a->h, a->nq, a->bh, a->do_stride_row, a->do_stride_bh, "dout",
                      qt)))
     return rc;

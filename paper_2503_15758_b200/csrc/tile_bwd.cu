@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int bh = blockIdx.y;
+  const int bh_kv = p.kv_group > 1 ? bh / p.kv_group : bh;  // GQA / MQA: shared k/v head
   const int kt_idx = blockIdx.x;
   auto bar = [&](int i) { return sb + L::OFF_BAR + 8 * i; };
   float* stat = reinterpret_cast<float*>(smem + L::OFF_STAT);
@@ -161,8 +162,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (lane == 0) {
         mbar_expect_tx(bar(L::B_KV), 2 * L::KV_BYTES);
         for (int s = 0; s < L::HS; ++s) {
-          tma_load_3d(sb + L::OFF_K + s * L::KSLAB, &tm_k, bar(L::B_KV), s * 64, kt.row0, bh);
-          tma_load_3d(sb + L::OFF_V + s * L::KSLAB, &tm_v, bar(L::B_KV), s * 64, kt.row0, bh);
+          tma_load_3d(sb + L::OFF_K + s * L::KSLAB, &tm_k, bar(L::B_KV), s * 64, kt.row0, bh_kv);
+          tma_load_3d(sb + L::OFF_V + s * L::KSLAB, &tm_v, bar(L::B_KV), s * 64, kt.row0, bh_kv);
         }
       }
       TileCursor cur;

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int bh = blockIdx.y;
+  const int bh_kv = p.kv_group > 1 ? bh / p.kv_group : bh;  // GQA / MQA: shared k/v head
   const int kt_idx = blockIdx.x;
   auto bar = [&](int i) { return sb + OFF_BAR + 8 * i; };
   float* stat = reinterpret_cast<float*>(smem + OFF_STAT);
@@ -118,8 +119,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
           mbar_expect_tx(bar(B_KV), 2 * TILE_B);
           for (int s = 0; s < 2; ++s) {
-            tma_load_3d(sb + OFF_K + s * SLAB, &tm_k, bar(B_KV), s * 64, kt.row0, bh);
-            tma_load_3d(sb + OFF_V + s * SLAB, &tm_v, bar(B_KV), s * 64, kt.row0, bh);
+            tma_load_3d(sb + OFF_K + s * SLAB, &tm_k, bar(B_KV), s * 64, kt.row0, bh_kv);
+            tma_load_3d(sb + OFF_V + s * SLAB, &tm_v, bar(B_KV), s * 64, kt.row0, bh_kv);
           }
         }
         // the LSE / delta rows of tile i+1 are loaded into registers while tile i

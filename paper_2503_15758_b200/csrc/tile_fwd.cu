@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   // q tiles vary fastest so co-resident CTAs share one head's K/V in L2;
   // within a head the heaviest (causal) tiles start first.
   const int bh = blockIdx.y;
+  const int bh_kv = p.kv_group > 1 ? bh / p.kv_group : bh;  // GQA / MQA: shared k/v head
   const int qt_idx = gridDim.x - 1 - blockIdx.x;
   const int rot = qt_idx;  // rotated key sweep (TileCursor)
   auto bar = [&](int i) { return sb + L::OFF_BAR + 8 * i; };
@@ -154,13 +155,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         mbar_expect_tx(bar(L::B_KFULL + ks), L::TILE_BYTES);
         for (int s = 0; s < L::SLABS; ++s)
           tma_load_3d(sb + L::OFF_K + ks * L::TILE_BYTES + s * L::SLAB, &tm_k,
-                      bar(L::B_KFULL + ks), s * 64, krow, bh);
+                      bar(L::B_KFULL + ks), s * 64, krow, bh_kv);
         if (++ks == L::KST) { ks = 0; kph ^= 1; }
         mbar_wait(bar(L::B_VEMPTY + vs), vph ^ 1);
         mbar_expect_tx(bar(L::B_VFULL + vs), L::TILE_BYTES);
         for (int s = 0; s < L::SLABS; ++s)
           tma_load_3d(sb + L::OFF_V + vs * L::TILE_BYTES + s * L::SLAB, &tm_v,
-                      bar(L::B_VFULL + vs), s * 64, krow, bh);
+                      bar(L::B_VFULL + vs), s * 64, krow, bh_kv);
         if (++vs == L::VST) { vs = 0; vph ^= 1; }
       }
     }

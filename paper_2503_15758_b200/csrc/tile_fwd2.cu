@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
   // tile pairs vary fastest (co-resident CTAs share one head's K/V in L2);
   // the heaviest causal pairs of a head start first.
   const int bh = blockIdx.y;
+  const int bh_kv = p.kv_group > 1 ? bh / p.kv_group : bh;  // GQA / MQA: shared k/v head
   const int pair = gridDim.x - 1 - blockIdx.x;
   auto bar = [&](int i) { return sb + L::OFF_BAR + 8 * i; };
   const uint32_t TM_O0 = 256, TM_O1 = 256 + HD;
@@ -272,14 +273,14 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
         mbar_expect_tx(bar(L::B_KFULL + ks), L::TILE_BYTES);
         for (int s = 0; s < L::SLABS; ++s)
           tma_load_3d(sb + L::OFF_K + ks * L::TILE_BYTES + s * L::SLAB, &tm_k,
-                      bar(L::B_KFULL + ks), s * 64, krow, bh);
+                      bar(L::B_KFULL + ks), s * 64, krow, bh_kv);
         if (++ks == L::KST) { ks = 0; kph ^= 1; }
         F2_WAIT(bar(L::B_VEMPTY + vs), vph ^ 1);
         TR(46, j);
         mbar_expect_tx(bar(L::B_VFULL + vs), L::TILE_BYTES);
         for (int s = 0; s < L::SLABS; ++s)
           tma_load_3d(sb + L::OFF_V + vs * L::TILE_BYTES + s * L::SLAB, &tm_v,
-                      bar(L::B_VFULL + vs), s * 64, krow, bh);
+                      bar(L::B_VFULL + vs), s * 64, krow, bh_kv);
         if (++vs == L::VST) { vs = 0; vph ^= 1; }
       }
     } else if (warp == 1 && n_tiles > 0) {

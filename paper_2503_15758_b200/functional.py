@@ -32,27 +32,49 @@ class _TileAttention(torch.autograd.Function):
 
 def attention_backward(q, k, v, o, lse, do, causal: bool, scale: float,
                        dq_acc: torch.Tensor | None = None):
-    """(dq, dk, dv) in bf16 for [bh, n, h] operands."""
+    """(dq, dk, dv) in bf16 for [bh, n, h] operands (k/v may have bh / g
+    heads: GQA / MQA, their gradients summed over each group of g query
+    heads in fp32)."""
     delta = ops.bwd_preprocess(o, do)
     if dq_acc is None:
         dq_acc = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
     else:
         dq_acc.zero_()
+    group = q.shape[0] // k.shape[0]
     dq_acc, dk, dv = ops.tile_backward(q, k, v, do, lse, delta, causal=causal, scale=scale,
-                                       dq_acc=dq_acc, dkv_dtype=torch.bfloat16)
+                                       dq_acc=dq_acc,
+                                       dkv_dtype=torch.bfloat16 if group == 1 else torch.float32)
+    if group > 1:
+        dk, dv = (t.view(k.shape[0], group, *t.shape[1:]).sum(1).to(torch.bfloat16)
+                  for t in (dk, dv))
     dq = ops.bwd_finalize(dq_acc, scale, dtype=torch.bfloat16)
     return dq, dk, dv
 
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = False,
               scale: float | None = None) -> torch.Tensor:
-    """softmax(scale q k^T [+ causal]) v for q/k/v of shape [B, M, N, H] or
-    [BH, N, H], bf16, on one B200.  scale defaults to 1/sqrt(H)."""
-    if q.dim() not in (3, 4) or q.shape != k.shape or k.shape != v.shape:
+    """softmax(scale q k^T [+ causal]) v for q of shape [B, M, N, H] or
+    [BH, N, H], bf16, on one B200.  k/v have the same shape, or M_kv heads
+    with M_kv dividing M (grouped-query / multi-query attention: query head
+    m reads k/v head m // (M / M_kv)).  scale defaults to 1/sqrt(H)."""
+    if q.dim() not in (3, 4) or k.shape != v.shape or k.dim() != q.dim():
+        raise ShapeError(f"q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)} do not conform")
+    hd = 1 if q.dim() == 4 else 0
+    if (q.shape[:hd] != k.shape[:hd] or q.shape[hd + 1:] != k.shape[hd + 1:]
+            or k.shape[hd] < 1 or q.shape[hd] % k.shape[hd]):
         raise ShapeError(f"q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)} do not conform")
     h = q.shape[-1]
     if scale is None:
         scale = h ** -0.5
+    hp = 64 if h <= 64 else 128
+    if h > 128:
+        raise ShapeError(f"head dim {h} > 128 is not supported")
+    if h != hp:
+        # other head dims (the reference's 80 / 96 presets, costmodel.py:73-79)
+        # run zero-padded: zero columns add nothing to q k^T, and the padded
+        # output / gradient columns are sliced off (exact)
+        pad = lambda x: torch.nn.functional.pad(x, (0, hp - h))  # noqa: E731
+        return attention(pad(q), pad(k), pad(v), causal, scale)[..., :h]
     shp = q.shape
     if q.dim() == 4:
         q, k, v = (x.reshape(-1, x.shape[2], h) for x in (q, k, v))

@@ -133,6 +133,14 @@ def launches() -> int:
     return LAUNCHES[0]
 
 
+def _kv_group(bh: int, k: torch.Tensor) -> int:
+    """Query heads per key/value head (GQA / MQA)."""
+    bk = k.shape[0] if k.dim() == 3 else 0
+    if bk < 1 or bh % bk:
+        raise ShapeError(f"{bk} key/value heads do not divide {bh} query heads")
+    return bh // bk
+
+
 def _stream(t: torch.Tensor) -> int:
     LAUNCHES[0] += 1
     return torch.cuda.current_stream(t.device).cuda_stream
@@ -166,7 +174,8 @@ def tile_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: b
                  k_index: TokenIndex | None = None, out: torch.Tensor | None = None,
                  lse: torch.Tensor | None = None, out_dtype: torch.dtype = torch.float32,
                  accumulate: bool = False):
-    """Partial attention of q against exactly the keys in k/v.
+    """Partial attention of q against exactly the keys in k/v.  k/v may hold
+    fewer heads than q (GQA / MQA): query head b reads k/v head b // group.
 
     Returns (o, lse): o [bh, nq, h] (fp32 normalised partial, or bf16 final),
     lse [bh, nq] fp32, -inf where a row attended nothing.  With accumulate,
@@ -178,7 +187,8 @@ def tile_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: b
     _check3("v", v)
     bh, nq, h = q.shape
     nk = k.shape[1]
-    if k.shape != (bh, nk, h) or v.shape != (bh, nk, h):
+    group = _kv_group(bh, k)
+    if k.shape != (bh // group, nk, h) or v.shape != k.shape:
         raise ShapeError(f"q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)} do not conform")
     qi = q_index if q_index is not None else TokenIndex.contiguous(nq)
     ki = k_index if k_index is not None else TokenIndex.contiguous(nk)
@@ -212,6 +222,7 @@ def tile_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: b
     a.o_dtype = _dtype_code(out.dtype)
     a.accumulate = int(bool(accumulate))
     a.q_map, a.k_map = qi.to_c(), ki.to_c()
+    a.kv_group = group
     _lib.check(lib.a2d_tile_fwd(a, _stream(q)), "a2d_tile_fwd")
     return out, lse
 
@@ -239,14 +250,16 @@ def tile_backward(q, k, v, dout, lse, delta, *, causal: bool, scale: float,
     GLOBAL (lse, delta) statistics of those rows (attention.py:225-257).
 
     dq_acc (fp32, unscaled dS K) is accumulated into; dk (scaled) and dv are
-    written.  Returns (dq_acc, dk, dv).
+    written, one per QUERY head (with GQA the caller sums each group).
+    Returns (dq_acc, dk, dv).
     """
     lib = _lib.load()
     for name, t in (("q", q), ("k", k), ("v", v), ("dout", dout)):
         _check3(name, t)
     bh, nq, h = q.shape
     nk = k.shape[1]
-    if k.shape != (bh, nk, h) or v.shape != (bh, nk, h) or dout.shape != q.shape:
+    group = _kv_group(bh, k)
+    if k.shape != (bh // group, nk, h) or v.shape != k.shape or dout.shape != q.shape:
         raise ShapeError("q/k/v/dout do not conform")
     if lse.shape != (bh, nq) or delta.shape != (bh, nq):
         raise ShapeError("lse / delta must be [bh, nq]")
@@ -280,6 +293,7 @@ def tile_backward(q, k, v, dout, lse, delta, *, causal: bool, scale: float,
     a.scale = float(scale)
     a.dkv_dtype = _dtype_code(dk.dtype)
     a.q_map, a.k_map = qi.to_c(), ki.to_c()
+    a.kv_group = group
     _lib.check(lib.a2d_tile_bwd(a, _stream(q)), "a2d_tile_bwd")
     return dq_acc, dk, dv
 

@@ -310,3 +310,49 @@ def test_no_uninitialised_reads_and_deterministic(ops, h, array_mode):
                 assert rel_fro(a, b) < 1e-5
             else:
                 assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("m,m_kv", [(8, 2), (4, 1)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_grouped_query_attention_fwd_bwd(ops, m, m_kv, causal):
+    """GQA / MQA (PAPER.md:951-955): query head j reads k/v head j // (m / m_kv)
+    inside the kernels (kv_group); dK / dV are summed over each group."""
+    from paper_2503_15758_b200 import functional
+    from gpu_util import ref_attention_grad
+    b, n, h = 2, 384, 128
+    q, do = uniform((b, m, n, h), 71), uniform((b, m, n, h), 72)
+    k, v = uniform((b, m_kv, n, h), 73), uniform((b, m_kv, n, h), 74)
+    scale = h ** -0.5
+    qg, kg, vg = (x.clone().requires_grad_(True) for x in (q, k, v))
+    o = functional.attention(qg, kg, vg, causal=causal, scale=scale)
+    o.backward(do)
+    g = m // m_kv
+    rep = lambda x: x.repeat_interleave(g, dim=1).reshape(b * m, n, h)  # noqa: E731
+    want_o, _ = ref_attention(q.reshape(b * m, n, h), rep(k), rep(v), causal, scale)
+    assert rel_fro(o.reshape(b * m, n, h), want_o) < REL_TOL
+    wq, wk, wv = ref_attention_grad(q.reshape(b * m, n, h), rep(k), rep(v),
+                                    do.reshape(b * m, n, h), causal, scale)
+    wk = wk.reshape(b, m_kv, g, n, h).sum(2)
+    wv = wv.reshape(b, m_kv, g, n, h).sum(2)
+    assert rel_fro(qg.grad.reshape(b * m, n, h), wq) < REL_TOL
+    assert rel_fro(kg.grad, wk) < REL_TOL
+    assert rel_fro(vg.grad, wv) < REL_TOL
+
+
+@pytest.mark.parametrize("h", [80, 96])
+def test_other_head_dims_zero_padded(ops, h):
+    """The reference's H=80 / 96 presets (costmodel.py:73-79) through the
+    drop-in: exact zero padding to 128."""
+    from paper_2503_15758_b200 import functional
+    from gpu_util import ref_attention_grad
+    bh, n = 3, 256
+    q, k, v, do = (uniform((bh, n, h), 80 + i) for i in range(4))
+    scale = h ** -0.5
+    qg, kg, vg = (x.clone().requires_grad_(True) for x in (q, k, v))
+    o = functional.attention(qg, kg, vg, causal=True, scale=scale)
+    o.backward(do)
+    want_o, _ = ref_attention(q, k, v, True, scale)
+    assert o.shape == q.shape and rel_fro(o, want_o) < REL_TOL
+    wq, wk, wv = ref_attention_grad(q, k, v, do, True, scale)
+    for got, want in ((qg.grad, wq), (kg.grad, wk), (vg.grad, wv)):
+        assert rel_fro(got, want) < REL_TOL
