@@ -293,8 +293,14 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------------------------------------------------------- e2e
     e2e = None
-    if world == 1 and not args.no_e2e:
-        hosts = [torch.empty((B, M, N, H), dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+    if not args.no_e2e:
+        # 1 GPU: functional.attention on [B, M, N, H]; N GPUs: each rank's shard
+        # [N/P, B*M, H] (column-major cyclic / ring layout) through the
+        # strategies' autograd entry point attention2d(q, k, v, plan)
+        shape = (B, M, N, H) if world == 1 else (L, BH, H)
+        if world > 1:
+            from paper_2503_15758_b200.strategies import attention2d
+        hosts = [torch.empty(shape, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
         for t in hosts:
             t.uniform_(-1, 1)
         res = torch.empty((1,), dtype=torch.float32).pin_memory()
@@ -304,7 +310,7 @@ def run_ours(args, rank, world, local_rank):
         # loop's data pipeline would run it; every step's copies and its loss
         # read-back stay inside the timed region.
         cs = torch.cuda.Stream(device=dev)
-        bufs = [[torch.empty((B, M, N, H), dtype=torch.bfloat16, device=dev) for _ in range(4)]
+        bufs = [[torch.empty(shape, dtype=torch.bfloat16, device=dev) for _ in range(4)]
                 for _ in range(2)]
         ready = [torch.cuda.Event() for _ in range(2)]
         done = [torch.cuda.Event() for _ in range(2)]
@@ -325,7 +331,10 @@ def run_ours(args, rank, world, local_rank):
                 h2d(i + 1)
             qd, kd, vd = (t.detach().requires_grad_(True) for t in bufs[s_][:3])
             dod = bufs[s_][3]
-            out = functional.attention(qd, kd, vd, causal=True, scale=scale)
+            if world == 1:
+                out = functional.attention(qd, kd, vd, causal=True, scale=scale)
+            else:
+                out = attention2d(qd, kd, vd, plan)
             out.backward(dod)
             loss = (out.float() * dod.float()).sum(dtype=torch.float32)
             res.copy_(loss.reshape(1), non_blocking=True)
@@ -338,19 +347,25 @@ def run_ours(args, rank, world, local_rank):
                 e2e_step(i, i + 1 < k)
 
         run_steps(2)
-        torch.cuda.synchronize()
+        barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         run_steps(args.steps)
         b.record(stream)
-        torch.cuda.synchronize()
+        barrier()
         ems = a.elapsed_time(b) / args.steps
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
         e2e = {"value": fl_step / (ems / 1e3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in hosts),
-               "d2h_bytes_per_step": 4, "ms_per_step": ems,
-               "path": "paper_2503_15758_b200.functional.attention (autograd); pinned host "
-                       "q/k/v/dO copied to HBM every step on a copy stream (step i+1's "
-                       "copy overlaps step i's compute) and the loss scalar read back"}
+               "h2d_bytes_per_step": world * sum(t.numel() * t.element_size() for t in hosts),
+               "d2h_bytes_per_step": 4 * world, "ms_per_step": ems,
+               "path": ("paper_2503_15758_b200.functional.attention" if world == 1 else
+                        f"paper_2503_15758_b200.strategies.attention2d ({args.strategy}, per-rank "
+                        "shards)") + " (autograd); pinned host q/k/v/dO copied to HBM every step "
+                       "on a copy stream (step i+1's copy overlaps step i's compute) and the loss "
+                       "scalar read back; max over ranks"}
         del bufs
         del hosts
 

@@ -110,6 +110,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   TileRange qr;
   query_range(p.q_map, p.nq, causal, kt.gmin, qr, TILE);
   const int n_tiles = qr.total;
+#ifdef A2D_X_NOROT
+  const int qrot = causal ? 0 : kt_idx;
+#else
+  const int qrot = kt_idx;  // rotated q sweep: co-resident CTAs reduce into different dQ rows
+#endif
 
   if (warp < 4) {
     regs_dec<72>();
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // the LSE / delta rows of tile i+1 are loaded into registers while tile i
         // is in flight, so their global-load latency never gates S_{i+1}
         TileCursor cur;
-        cur.start(qr, kt_idx);
+        cur.start(qr, qrot);
         float l2n[4], dln[4];
         auto load_stats = [&](int qrow) {
 #pragma unroll
@@ -280,10 +285,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     // for affine maps are computed 32 tiles at a time, one tile per lane,
     // and broadcast with one shuffle per tile; explicit index arrays keep a
     // per-tile path.
-    const int rot0 = n_tiles > 0 ? kt_idx % n_tiles : 0;
+    const int rot0 = n_tiles > 0 ? qrot % n_tiles : 0;
     uint32_t my_info = 0;
     TileCursor cur;
-    if (!affine) cur.start(qr, kt_idx);
+    if (!affine) cur.start(qr, qrot);
     for (int i = 0; i < n_tiles; ++i) {
       const int qs = i & 1;
       int first = 0;  // first visible query column of this key row
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
     int round = 0;
     TileCursor cur;
-    cur.start(qr, kt_idx);
+    cur.start(qr, qrot);
     for (int i = 0; i < n_tiles; ++i, cur.next(qr)) {
       const int qrow = cur.row0(p.q_map);
       mbar_wait(bar(B_DQFULL), i & 1);
