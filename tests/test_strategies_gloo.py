@@ -154,7 +154,9 @@ def test_matches_reference_strategy_golden(name, causal):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,grid", [("attn2d_no", (2, 2)), ("attn2d_o", (2, 2)),
-                                       ("attn2d_o", (1, 2)), ("ring", None)])
+                                       ("attn2d_o", (1, 2)), ("ring", None),
+                                       ("attn2d_no", (2, 1)), ("attn2d_no", (2, 4)),
+                                       ("attn2d_o", (2, 4))])
 def test_strategies_on_cuda_kernels(name, grid):
     """Four gloo ranks whose every tile / merge / preprocess / finalize call
     runs on the sm_100a kernels (tests/gpu_bridge.py): the distributed
