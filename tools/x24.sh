@@ -1,0 +1,2 @@
+A2D_LIB_PATH=xlib/lib_statpipe.so timeout 300 python -m pytest tests/test_gpu_tile.py -m gpu -x -q -k backward 2>&1 | tail -1 > gpurun_out/x24.txt
+bash tools/run_ab.sh x24 "statpipe" "bwd 32768 32 128 1" "bwd 131072 32 128 1" "bwd 32768 32 128 0"
