@@ -439,68 +439,102 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
       }
 #endif
       float s[NC];
+      auto load_s = [&]() {  // S_t(j) row from TMEM, causal / ragged columns masked
 #pragma unroll
-      for (int c = 0; c < NC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
-      tmem_wait_ld();
+        for (int c = 0; c < NC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
+        tmem_wait_ld();
+        if (partial) {
+#pragma unroll
+          for (int jj = 0; jj < NC; ++jj)
+            if (jj > lim) s[jj] = -INFINITY;
+        }
+      };
+      load_s();
       TR(1 * 8 + t * 4 + quarter, j);
-      if (partial) {
-#pragma unroll
-        for (int jj = 0; jj < NC; ++jj)
-          if (jj > lim) s[jj] = -INFINITY;
-      }
-      float mx = rowmax<NC>(s) * sl2;
-      if constexpr (CS == 2) {
-        // both halves of a row need one common max: exchange through smem.
-        // One slot per (tile, half, row) suffices: the partner reads it
-        // before arriving on PFULL(j), and this slot is rewritten only after
-        // S(j+1), i.e. after PV(j) consumed both halves' P.
-        xch[h * 128 + row] = mx;
-        named_bar_sync(xbar, 64);
-        mx = fmaxf(mx, xch[(h ^ 1) * 128 + row]);
-      }
-      const float m_new = fmaxf(m_run, mx);
       float alpha = 1.f;
-      if (m_new > m_run + kRescaleThreshold) {
-        alpha = ex2(m_run - m_new);
-        m_run = m_new;
-      }
-      const float mb = (m_run == -INFINITY) ? 0.f : m_run;
-#ifdef F2X_SEQ
-      // Experiment (-DF2X_SEQ, measured 2% slower): the two tile warpgroups
-      // take turns on the exponential phase: WG1's exp(j) follows
-      // WG0's exp(j), WG0's exp(j+1) follows WG1's exp(j).  Generations of
-      // the two named barriers cannot mix: a warp re-arrives only after the
-      // other warpgroup has passed the barrier it arrived on.
-      if (CS == 1 && (t == 1 || j > 0)) named_bar_sync(t == 0 ? 9 : 10, 256);
-#endif
-      TR(2 * 8 + t * 4 + quarter, j);
       uint32_t pk[NC / 2];
-      float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-      const float2 sc = make_float2(sl2, sl2), nb = make_float2(-mb, -mb);
-      if (partial) {  // masked entries are -inf: the exact MUFU path keeps them 0
+      const float2 sc = make_float2(sl2, sl2);
+      // exponentials of this tile against the running max (P in pk, returns
+      // the tile's share of the denominator)
+      auto exps = [&](float mbase) -> float {
+        float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+        const float2 nb = make_float2(-mbase, -mbase);
+        if (partial) {  // masked entries are -inf: the exact MUFU path keeps them 0
 #pragma unroll
-        for (int jj = 0; jj < NC; jj += 2) {
-          const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
-          const float2 e = make_float2(XEX2(x.x), XEX2(x.y));
-          acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
-          pk[jj / 2] = pack_bf16(e.x, e.y);
+          for (int jj = 0; jj < NC; jj += 2) {
+            const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
+            const float2 e = make_float2(XEX2(x.x), XEX2(x.y));
+            acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
+            pk[jj / 2] = pack_bf16(e.x, e.y);
+          }
+        } else {  // a quarter of the exponentials on the FMA pipe (MUFU offload)
+#pragma unroll
+          for (int jj = 0; jj < NC; jj += 2) {
+            const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
+            float2 e;
+            if (F2_POLY(jj)) e = exp2_poly2(x);
+            else e = make_float2(XEX2(x.x), XEX2(x.y));
+            acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
+            pk[jj / 2] = pack_bf16(e.x, e.y);
+          }
         }
-      } else {  // a quarter of the exponentials on the FMA pipe (MUFU offload)
-#pragma unroll
-        for (int jj = 0; jj < NC; jj += 2) {
-          const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
-          float2 e;
-          if (F2_POLY(jj)) e = exp2_poly2(x);
-          else e = make_float2(XEX2(x.x), XEX2(x.y));
-          acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
-          pk[jj / 2] = pack_bf16(e.x, e.y);
+        const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+        const float2 a = fadd2(a01, a23);
+        return a.x + a.y;
+      };
+      auto move_max = [&]() {  // exact running max of this tile (log2 domain)
+        float mx = rowmax<NC>(s) * sl2;
+        if constexpr (CS == 2) {
+          // both halves of a row need one common max: exchange through smem.
+          // One slot per (tile, half, row) suffices: the partner reads it
+          // before arriving on PFULL(j), and this slot is rewritten only after
+          // S(j+1), i.e. after PV(j) consumed both halves' P.
+          xch[h * 128 + row] = mx;
+          named_bar_sync(xbar, 64);
+          mx = fmaxf(mx, xch[(h ^ 1) * 128 + row]);
+        }
+        return mx;
+      };
+#ifdef F2X_ROWMAX
+      {  // classic: row max every tile, moved when it grows by > 2^8
+        const float m_new = fmaxf(m_run, move_max());
+        if (m_new > m_run + kRescaleThreshold) {
+          alpha = ex2(m_run - m_new);
+          m_run = m_new;
         }
       }
-      const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-      const float2 a = fadd2(a01, a23);
-      l_run = l_run * alpha + (a.x + a.y);
-#ifdef F2X_SEQ
-      if (CS == 1 && (t == 0 || j + 1 < n_tiles)) named_bar_arrive(t == 0 ? 10 : 9, 256);
+      float tsum = exps(m_run == -INFINITY ? 0.f : m_run);
+#else
+      // No row max in the steady state: P = 2^(x - m_run) with the max of the
+      // row's first visible tile.  Values above 1 are exact in bf16 / fp32
+      // (relative precision), so the max only has to move when a tile's sum
+      // nears overflow (>= 2^64, or non-finite) — then it is recomputed
+      // exactly and the tile redone.  Saves the 128-wide max tree per tile.
+      if (CS == 2 || __any_sync(0xffffffffu, m_run == -INFINITY)) {
+        const float m_new = fmaxf(m_run, move_max());
+        if (m_new > m_run) {
+          alpha = (m_run == -INFINITY) ? 1.f : ex2(m_run - m_new);
+          m_run = m_new;
+        }
+      }
+      float tsum = exps(m_run == -INFINITY ? 0.f : m_run);
+      if (__any_sync(0xffffffffu, !(tsum < 0x1p64f))) {  // rare: S is still in TMEM
+        load_s();
+        const float m_new = fmaxf(m_run, move_max());
+        if (m_new > m_run) {
+          alpha *= (m_run == -INFINITY) ? 1.f : ex2(m_run - m_new);
+          m_run = m_new;
+        }
+        tsum = exps(m_run == -INFINITY ? 0.f : m_run);
+      }
+#endif
+      l_run = l_run * alpha + tsum;
+#ifndef F2X_ROWMAX
+      if (l_run > 0x1p96f) {  // keep the denominator far from fp32 overflow
+        l_run *= 0x1p-64f;
+        alpha *= 0x1p-64f;
+        m_run += 64.f;
+      }
 #endif
       TR(3 * 8 + t * 4 + quarter, j);
       // P_t(j), this half's keys, over S_t columns that are already consumed

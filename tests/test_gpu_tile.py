@@ -356,3 +356,25 @@ def test_other_head_dims_zero_padded(ops, h):
     wq, wk, wv = ref_attention_grad(q, k, v, do, True, scale)
     for got, want in ((qg.grad, wq), (kg.grad, wk), (vg.grad, wv)):
         assert rel_fro(got, want) < REL_TOL
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_forward_growing_scores_move_the_running_max(ops, causal):
+    """Scores that grow by ~2^100 along the key sweep: the forward's running
+    max (taken from the first visible tile, moved only when a tile's sum
+    nears overflow) must re-base exactly; compared with the fp32 reference."""
+    bh, n, h = 2, 1024, 64
+    g = torch.Generator(device="cpu").manual_seed(7)
+    u = torch.randn((h,), generator=g)
+    u = u / u.norm()
+    a = torch.linspace(0.5, 1.0, n)[:, None]                  # query rows
+    b = torch.linspace(-10.0, 90.0, n)[:, None]               # key rows: growing scores
+    noise = lambda: 0.05 * torch.randn((n, h), generator=g)   # noqa: E731
+    q = (a * u + noise()).expand(bh, n, h).contiguous().to("cuda", torch.bfloat16)
+    k = (b * u + noise()).expand(bh, n, h).contiguous().to("cuda", torch.bfloat16)
+    v = uniform((bh, n, h), 91)
+    o, lse = ops.tile_forward(q, k, v, causal=causal, scale=1.0, out_dtype=torch.float32)
+    want_o, want_lse = ref_attention(q, k, v, causal, 1.0)
+    assert torch.isfinite(o).all() and torch.isfinite(lse).all()
+    assert rel_fro(o, want_o) < REL_TOL
+    assert max_abs(lse, want_lse) < 1e-3 * max(1.0, float(want_lse.abs().max()))
