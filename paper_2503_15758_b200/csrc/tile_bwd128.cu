@@ -30,6 +30,15 @@
 #include "tiles.cuh"
 #include "kernels.h"
 
+// exponential pairs of the P phase evaluated on the FMA-pipe polynomial
+#if defined(B2X_POLY0)
+#define B_POLY(c) false
+#elif defined(B2X_POLY1OF8)
+#define B_POLY(c) ((((c) >> 1) & 7) == 7)
+#else
+#define B_POLY(c) ((((c) >> 1) & 3) == 3)
+#endif
+
 namespace a2d {
 namespace {
 
@@ -42,9 +51,20 @@ constexpr int OFF_V = OFF_K + TILE_B;
 constexpr int OFF_Q = OFF_V + TILE_B;      // 2 stages
 constexpr int OFF_DO = OFF_Q + 2 * TILE_B;
 constexpr int OFF_DS = OFF_DO + TILE_B;
-constexpr int STG = 4 * 32 * 128;          // one staging buffer: 4 slabs of [32 q][32 h] fp32
-constexpr int OFF_DQ = OFF_DS + TILE_B;    // 2 buffers
-constexpr int OFF_STAT = OFF_DQ + 2 * STG; // [2][2][128] fp32
+// dQ staging: DQ_BUFS buffers of DQ_ROWS query rows x 128 fp32 (32 KB in all),
+// so up to DQ_BUFS TMA bulk reduce-adds are in flight per CTA.  The per-SM
+// bulk-reduce throughput (~20 B/clk measured) is what bounds this kernel:
+// 4 x 16-row buffers measured 1-3% faster than 2 x 32, 8 x 8 16% slower, and
+// moving rows to red.global.add from registers is slower still.
+#ifndef B2_DQ_BUFS
+#define B2_DQ_BUFS 4
+#endif
+constexpr int DQ_BUFS = B2_DQ_BUFS;
+constexpr int DQ_ROWS = 64 / DQ_BUFS;
+constexpr int DQ_ROUNDS = 128 / DQ_ROWS;
+constexpr int DQ_BUF_BYTES = DQ_ROWS * 128 * 4;
+constexpr int OFF_DQ = OFF_DS + TILE_B;
+constexpr int OFF_STAT = OFF_DQ + DQ_BUFS * DQ_BUF_BYTES;  // [2][2][128] fp32
 constexpr int OFF_BAR = OFF_STAT + 2 * 2 * 128 * 4;
 enum {
   B_KV, B_QFULL0, B_QFULL1, B_QEMPTY0, B_QEMPTY1, B_DOFULL, B_DOEMPTY, B_SFULL, B_PREADY,
@@ -349,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < 64; c += 2) {
           const float2 x = ffma2(make_float2(pr[c], pr[c + 1]), sc,
                                  make_float2(-s_lse[c], -s_lse[c + 1]));
-          const float2 e = (((c >> 1) & 3) == 3) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          const float2 e = B_POLY(c) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           pk[c >> 1] = pack_bf16(e.x, e.y);
         }
       } else {
@@ -460,15 +480,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       mbar_arrive(bar(B_DQFREE));
 #pragma unroll
-      for (int r = 0; r < 4; ++r, ++round) {
-        const uint32_t buf = sb + OFF_DQ + (round & 1) * STG;
-        if (h == 0) bulk_wait_group_read<1>();  // this buffer's previous reduce has read it
+      for (int r = 0; r < DQ_ROUNDS; ++r, ++round) {
+        const uint32_t buf = sb + OFF_DQ + (round % DQ_BUFS) * DQ_BUF_BYTES;
+        // this buffer's previous reduce has read it
+        if (h == 0) bulk_wait_group_read<DQ_BUFS - 1>();
         named_bar_sync(1, 128);
-        // row-major [32 q][128 h] fp32: a warp's 32 head dims are one 128 B row
+        // row-major [DQ_ROWS q][128 h] fp32: a warp's 32 head dims are one 128 B row
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
+        for (int q = 0; q < DQ_ROWS; ++q) {
           const uint32_t addr = buf + q * 512 + h * 4;
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v[32 * r + q]) : "memory");
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v[DQ_ROWS * r + q]) : "memory");
         }
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
@@ -477,7 +498,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #else
         if (h == 0) {
 #endif
-          tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + 32 * r, bh);
+          tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);
           bulk_commit_group();
         }
       }
@@ -507,7 +528,7 @@ int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUten
     configured[dev & 63] = true;
   }
   CUtensorMap tdq;
-  int rc = make_map_f32_dq_flat(&tdq, a.dq_acc, 128, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh, 32);
+  int rc = make_map_f32_dq_flat(&tdq, a.dq_acc, 128, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh, DQ_ROWS);
   if (rc) return rc;
   const int k_tiles = (a.k_map.mode == A2D_IDX_AFFINE && a.k_map.nblocks > 1)
                           ? a.k_map.nblocks * (a.k_map.rows_per_block / TILE)
