@@ -109,7 +109,7 @@ class ClockSampler:
 # CPU legs: the oracle port of the reference's numpy kernels
 # --------------------------------------------------------------------------
 
-def cpu_sample(n_cpu=4096, h=128, causal=True, budget_s=12.0, max_heads=8):
+def cpu_sample(n_cpu=4096, h=128, causal=True, budget_s=12.0, max_heads=32):
     """Time the reference algorithm (oracle port of kernels/numpy_backend.py,
     fwd + bwd through flash_attn_forward / finalize / flash_attn_backward) on
     a bounded sample: whole heads of N=n_cpu until the budget is spent."""
