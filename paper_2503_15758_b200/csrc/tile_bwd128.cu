@@ -495,6 +495,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         named_bar_sync(1, 128);
 #ifdef A2D_X_NO_DQ
         if (false) {
+#elif defined(A2D_X_HALF_DQ)
+        if (h == 0 && r < DQ_ROUNDS / 2) {
 #else
         if (h == 0) {
 #endif
