@@ -186,3 +186,35 @@ def test_attn2d_comm_volume_identity():
         bwd += 0 if diag else 2 * L * heads * h * 2
         assert r["fwd_bytes"] == fwd, (rank, r["fwd_bytes"], fwd)
         assert r["bwd_bytes"] == bwd, (rank, r["bwd_bytes"], bwd)
+
+
+def _relayout_worker(rank, world, port, grid, outdir):
+    sys.path.insert(0, str(HERE.parent))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_15758_b200.layouts import Grid2D
+        from paper_2503_15758_b200.strategies import GridComm
+        from paper_2503_15758_b200.strategies.relayout import from_cyclic, to_cyclic
+        g = Grid2D(*grid)
+        comm = GridComm(g)
+        n, L = 64 * world, 64
+        full = torch.arange(n * 3, dtype=torch.float32).reshape(n, 3)
+        mine = full[rank * L:(rank + 1) * L].clone()
+        cyc = to_cyclic(mine, comm)
+        want = full[torch.as_tensor(g.owned(n, *g.coord(rank)))]
+        assert torch.equal(cyc, want), (rank, cyc[:4], want[:4])
+        back = from_cyclic(cyc, comm)
+        assert torch.equal(back, mine)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("grid", [(2, 1), (2, 2), (1, 4)])
+def test_layer_boundary_relayout_roundtrip(grid):
+    """Sequence-parallel contiguous chunks <-> column-major cyclic shards
+    with one all_to_all each way."""
+    world = grid[0] * grid[1]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_relayout_worker, args=(world, _free_port(), grid, d), nprocs=world, join=True)
