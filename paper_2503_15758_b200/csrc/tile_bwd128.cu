@@ -500,7 +500,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #else
         if (h == 0) {
 #endif
+#ifdef B2X_DQ_EVICT_LAST
+          tma_reduce_add_3d_g_hint(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh, l2_policy_evict_last());
+#else
           tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);
+#endif
           bulk_commit_group();
         }
       }
