@@ -378,3 +378,52 @@ def test_forward_growing_scores_move_the_running_max(ops, causal):
     assert torch.isfinite(o).all() and torch.isfinite(lse).all()
     assert rel_fro(o, want_o) < REL_TOL
     assert max_abs(lse, want_lse) < 1e-3 * max(1.0, float(want_lse.abs().max()))
+
+
+@pytest.mark.parametrize("n,bh", [(32768, 2), (131072, 1)])
+def test_full_size_row_and_key_sampled_parity(ops, n, bh):
+    """C2 (N=32768) and the metric size (N=131072), H=128, causal, with fewer
+    heads, against an fp64 reference evaluated chunk-wise on the GPU (SURVEY
+    §8c "large N" protocol): LSE of every row, O / dQ on sampled query rows,
+    dK / dV on sampled key rows."""
+    from paper_2503_15758_b200 import functional
+    h = 128
+    scale = h ** -0.5
+    q, k, v, do = (uniform((bh, n, h), 120 + i) for i in range(4))
+    qg, kg, vg = (x.clone().requires_grad_(True) for x in (q, k, v))
+    o = functional.attention(qg, kg, vg, causal=True, scale=scale)
+    o.backward(do)
+    _, lse = ops.tile_forward(q, k, v, causal=True, scale=scale, out_dtype=torch.bfloat16)
+    qd, kd, vd, dod = (x.double() for x in (q, k, v, do))
+    kidx = torch.arange(n, device="cuda")
+    lse_ref = torch.empty((bh, n), dtype=torch.float64, device="cuda")
+    o_ref = torch.empty((bh, n, h), dtype=torch.float64, device="cuda")
+    for r0 in range(0, n, 2048):
+        s = torch.einsum("bqh,bkh->bqk", qd[:, r0:r0 + 2048], kd) * scale  # [bh, 2048, n]
+        s = s.masked_fill(kidx[None, None, :] > (r0 + torch.arange(2048, device="cuda"))[None, :, None],
+                          float("-inf"))
+        lse_ref[:, r0:r0 + 2048] = torch.logsumexp(s, -1)
+        o_ref[:, r0:r0 + 2048] = torch.einsum("bqk,bkh->bqh",
+                                              torch.exp(s - lse_ref[:, r0:r0 + 2048, None]), vd)
+    assert max_abs(lse, lse_ref) < LSE_TOL
+    delta_ref = (o_ref * dod).sum(-1)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    rows = torch.randint(0, n, (96,), generator=g).cuda()
+    keys = torch.randint(0, n, (96,), generator=g).cuda()
+    # sampled query rows: O and dQ
+    s = torch.einsum("bqh,bkh->bqk", qd[:, rows], kd) * scale
+    s = s.masked_fill(kidx[None, None, :] > rows[None, :, None], float("-inf"))
+    p = torch.exp(s - lse_ref[:, rows, None])
+    dp = torch.einsum("bqh,bkh->bqk", dod[:, rows], vd)
+    dq_ref = torch.einsum("bqk,bkh->bqh", p * (dp - delta_ref[:, rows, None]), kd) * scale
+    assert rel_fro(o[:, rows], o_ref[:, rows]) < REL_TOL
+    assert rel_fro(qg.grad[:, rows], dq_ref) < REL_TOL
+    # sampled key rows: dK and dV over every query
+    s = torch.einsum("bqh,bkh->bqk", qd, kd[:, keys]) * scale
+    s = s.masked_fill(keys[None, None, :] > kidx[None, :, None], float("-inf"))
+    p = torch.exp(s - lse_ref[:, :, None])
+    dp = torch.einsum("bqh,bkh->bqk", dod, vd[:, keys])
+    dk_ref = torch.einsum("bqk,bqh->bkh", p * (dp - delta_ref[:, :, None]), qd) * scale
+    dv_ref = torch.einsum("bqk,bqh->bkh", p, dod)
+    assert rel_fro(kg.grad[:, keys], dk_ref) < REL_TOL
+    assert rel_fro(vg.grad[:, keys], dv_ref) < REL_TOL
