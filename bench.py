@@ -176,9 +176,13 @@ def run_ours(args, rank, world, local_rank):
     _lib.load()
     N, M, H, B = args.seq_len, args.heads, 128, 1
     BH = B * M
-    causal = True
+    causal = not args.non_causal
     scale = H ** -0.5
     pr, pc = GRIDS.get(world, (1, world))
+    if args.grid:
+        pr, pc = (int(x) for x in args.grid.lower().split("x"))
+        if pr * pc != world:
+            raise SystemExit(f"--grid {args.grid} does not match {world} ranks")
     grid = Grid2D(pr, pc) if args.strategy in ("attn2d_no", "attn2d_o") else Grid2D(1, world)
     L = N // world
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -186,7 +190,7 @@ def run_ours(args, rank, world, local_rank):
     def rnd(shape):
         return torch.empty(shape, dtype=torch.bfloat16, device=dev).uniform_(-1, 1, generator=g)
 
-    fl_step = 3.5 * flops_fwd(B, M, H, N, causal)
+    fl_step = (1.0 if args.fwd_only else 3.5) * flops_fwd(B, M, H, N, causal)
     stream = torch.cuda.current_stream()
 
     # kernel-level events for the roofline of the dominant kernel (tile bwd)
@@ -209,6 +213,10 @@ def run_ours(args, rank, world, local_rank):
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
+            if args.fwd_only:
+                if record:
+                    kev["fwd"].append((e0, e1))
+                return
             delta = ops.bwd_preprocess(o, do)
             dq_acc.zero_()
             if record:
@@ -236,7 +244,8 @@ def run_ours(args, rank, world, local_rank):
 
         def step(record=False):
             o_p, saved = plan.forward(q, k, v)
-            plan.backward(saved, do)
+            if not args.fwd_only:
+                plan.backward(saved, do)
         dominant = "tile_bwd"
 
     def barrier():
@@ -271,6 +280,13 @@ def run_ours(args, rank, world, local_rank):
 
     peak_burst, peak_sus, hbm, peak_kind = measured_peaks()
     roof = None
+    if kev["fwd"] and not kev["bwd"]:  # --fwd-only: the tile forward dominates
+        kf = statistics.mean(a.elapsed_time(b) for a, b in kev["fwd"])
+        ach = flops_fwd(B, M, H, N, causal) / (kf / 1e3) / 1e12
+        roof = {"kernel": "tile_fwd (a2d_tile_fwd)", "bound": "tensor", "achieved": ach,
+                "peak": peak_sus, "peak_kind": f"bf16_tflops_sustained ({peak_kind})",
+                "unit": "TFLOP/s", "frac": ach / peak_sus, "traffic": None, "ms_per_launch": kf,
+                "flops_per_launch": flops_fwd(B, M, H, N, causal)}
     if kev["bwd"]:
         kb = statistics.mean(a.elapsed_time(b) for a, b in kev["bwd"])
         kf = statistics.mean(a.elapsed_time(b) for a, b in kev["fwd"])
@@ -293,7 +309,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------------------------------------------------------- e2e
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.fwd_only:
         # 1 GPU: functional.attention on [B, M, N, H]; N GPUs: each rank's shard
         # [N/P, B*M, H] (column-major cyclic / ring layout) through the
         # strategies' autograd entry point attention2d(q, k, v, plan)
@@ -374,14 +390,17 @@ def run_ours(args, rank, world, local_rank):
         cpu = cpu_sample()
 
     if rank == 0:
+        default = not (args.fwd_only or args.non_causal or args.grid)
+        mode = f"{'causal' if causal else 'non-causal'} {'fwd' if args.fwd_only else 'fwd+bwd'}"
         line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "metric": METRIC if default else f"attention {mode} TFLOP/s, N={N}, M={M}, H={H}",
+            "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic uniform[-1,1] bf16 (torch.Generator on device)",
-            "config": {"workload": f"exact causal attention fwd+bwd, N={N}, M={M}, H={H}, B=1, "
+            "config": {"workload": f"exact {mode} attention, N={N}, M={M}, H={H}, B=1, "
                                    f"bf16, grid {grid.pr}x{grid.pc} ({args.strategy})",
-                       "seq_len": N, "heads": M, "head_dim": H, "batch": B, "causal": True,
+                       "seq_len": N, "heads": M, "head_dim": H, "batch": B, "causal": causal,
                        "grid": f"{grid.pr}x{grid.pc}", "strategy": args.strategy,
                        "parallelism": f"2d{grid.pr}x{grid.pc}" if world > 1 else "1x1",
                        "flops_per_step": fl_step,
@@ -402,6 +421,9 @@ def main():
     ap.add_argument("--seq-len", type=int, default=131072)
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--head-chunks", type=int, default=4)
+    ap.add_argument("--grid", default=None, help="Pr x Pc override, e.g. 4x2 (C5 sweep)")
+    ap.add_argument("--fwd-only", action="store_true", help="forward only (C5 prefill)")
+    ap.add_argument("--non-causal", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
