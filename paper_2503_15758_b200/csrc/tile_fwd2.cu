@@ -514,15 +514,20 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
       // (relative precision), so the max only has to move when a tile's sum
       // nears overflow (>= 2^64, or non-finite) — then it is recomputed
       // exactly and the tile redone.  Saves the 128-wide max tree per tile.
-      if (CS == 2 || __any_sync(0xffffffffu, m_run == -INFINITY)) {
+      // (m_run is identical in both column halves of a row, so with CS == 2
+      // both warps take this branch together and meet in move_max's barrier)
+      if (__any_sync(0xffffffffu, m_run == -INFINITY)) {
         const float m_new = fmaxf(m_run, move_max());
         if (m_new > m_run) {
           alpha = (m_run == -INFINITY) ? 1.f : ex2(m_run - m_new);
           m_run = m_new;
         }
       }
+      TR(2 * 8 + t * 4 + quarter, j);
       float tsum = exps(m_run == -INFINITY ? 0.f : m_run);
-      if (__any_sync(0xffffffffu, !(tsum < 0x1p64f))) {  // rare: S is still in TMEM
+      bool ovf = __any_sync(0xffffffffu, !(tsum < 0x1p64f));
+      if constexpr (CS == 2) ovf = bar_red_or(xbar, 64, ovf);  // one decision for both halves
+      if (ovf) {  // rare: S is still in TMEM
         load_s();
         const float m_new = fmaxf(m_run, move_max());
         if (m_new > m_run) {
