@@ -315,11 +315,13 @@ A2D_DEV float2 fadd2(float2 a, float2 b) {
 // 2^x for finite x <= ~8 on the FMA/ALU pipes (MUFU offload): round-to-nearest
 // split x = n + f, f in [-0.5, 0.5], near-minimax cubic for 2^f (max rel err
 // 1.0e-4, far below the bf16 rounding of P), 2^n folded into the exponent.
-// Inputs below -126 flush towards 2^-126; -inf is NOT supported (masked
-// tiles use the MUFU path).
+// Inputs are clamped to [-126, 127]; -inf is NOT supported (masked tiles use
+// the MUFU path).
 A2D_DEV float2 exp2_poly2(float2 x) {
-  const float2 lo = make_float2(-126.f, -126.f);
-  x = make_float2(fmaxf(x.x, lo.x), fmaxf(x.y, lo.y));
+  // clamp to [-126, 127]: below, the result flushes towards 2^-126; above,
+  // it saturates at 2^127 (finite, so a caller's overflow guard still sees
+  // it — an unclamped large x would wrap the exponent field)
+  x = make_float2(fminf(fmaxf(x.x, -126.f), 127.f), fminf(fmaxf(x.y, -126.f), 127.f));
   const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
   const float2 t = fadd2(x, magic);
   const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));

@@ -427,3 +427,25 @@ def test_full_size_row_and_key_sampled_parity(ops, n, bh):
     dv_ref = torch.einsum("bqk,bqh->bkh", p, dod)
     assert rel_fro(kg.grad[:, keys], dk_ref) < REL_TOL
     assert rel_fro(vg.grad[:, keys], dv_ref) < REL_TOL
+
+
+@pytest.mark.parametrize("col", [270, 271, 300])
+def test_forward_single_huge_score_on_any_column(ops, col):
+    """One key whose score exceeds every earlier tile's by ~2^200, placed on
+    a column the forward evaluates with the FMA-pipe polynomial (270, 271)
+    or with MUFU (300): the overflow guard must catch it either way."""
+    bh, n, h = 1, 512, 64
+    g = torch.Generator(device="cpu").manual_seed(11)
+    u = torch.randn((h,), generator=g)
+    u = u / u.norm()
+    q = (u + 0.01 * torch.randn((n, h), generator=g))[None].contiguous()
+    k = (0.01 * torch.randn((n, h), generator=g))[None].contiguous()
+    k[0, col] = 140.0 * u
+    q, k = q.to("cuda", torch.bfloat16), k.to("cuda", torch.bfloat16)
+    v = uniform((bh, n, h), 93)
+    for causal in (False, True):
+        o, lse = ops.tile_forward(q, k, v, causal=causal, scale=1.0, out_dtype=torch.float32)
+        want_o, want_lse = ref_attention(q, k, v, causal, 1.0)
+        assert torch.isfinite(o).all() and torch.isfinite(lse).all()
+        assert rel_fro(o, want_o) < REL_TOL, (causal, rel_fro(o, want_o))
+        assert max_abs(lse, want_lse) < 1e-3 * max(1.0, float(want_lse.abs().max()))
