@@ -168,6 +168,15 @@ def test_strategies_on_cuda_kernels(name, grid):
     _run((name, grid, n, 64, 2, True, False, "gpu"), world)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["attn2d_no", "attn2d_o"])
+def test_c1_config_on_cuda_kernels(name):
+    """BASELINE config C1 exactly: B=1, M=4, N=2048, H=64, non-causal, on a
+    2x2 grid (four gloo ranks sharing the B200 through the kernel bridge),
+    against the dense oracle."""
+    _run((name, (2, 2), 2048, 64, 4, False, False, "gpu"), 4)
+
+
 def test_attn2d_comm_volume_identity():
     """Bytes leaving each rank equal the generalised volume identity
     (costmodel.py:120-136 with the LSE form and delta instead of O)."""
