@@ -128,10 +128,10 @@ class PartialAttn:
 
 
 def _padded_h(h: int) -> int:
-    if h <= 64:
-        return 64
+    """Head dim the kernels run: h rounded up to a multiple of 8 (16-byte
+    rows; the tiles zero-fill the rest of their 64 / 128 columns)."""
     if h <= 128:
-        return 128
+        return max(8, -(-h // 8) * 8)
     raise UnsupportedError(f"head dim {h} > 128 is not supported by the sm_100a tile")
 
 

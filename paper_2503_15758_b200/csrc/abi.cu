@@ -101,7 +101,7 @@ int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, l
 
 // Same accumulator, box h x box_rows x 1 without swizzle (row-major staging).
 int make_map_f32_dq_flat(CUtensorMap* m, const float* ptr, int h, int rows, int bh,
-                         long long s_row, long long s_bh, int box_rows) {
+                         long long s_row, long long s_bh, int box_rows, int box_cols) {
   if (reinterpret_cast<uintptr_t>(ptr) % 16) return set_error(A2D_EINVAL, "dq_acc must be 16-byte aligned");
   if ((s_row * 4) % 16 || (s_bh * 4) % 16)
     return set_error(A2D_EINVAL, "dq_acc strides must be multiples of 4 elements");
@@ -110,7 +110,8 @@ int make_map_f32_dq_flat(CUtensorMap* m, const float* ptr, int h, int rows, int 
   cuuint64_t dims[3] = {(cuuint64_t)h, (cuuint64_t)rows, (cuuint64_t)bh};
   cuuint64_t strides[2] = {(cuuint64_t)(s_row * 4), (cuuint64_t)(s_bh * 4)};
   if (bh == 1) strides[1] = (cuuint64_t)((long long)rows * s_row * 4);
-  cuuint32_t box[3] = {(cuuint32_t)h, (cuuint32_t)box_rows, 1};
+  // box_cols may exceed h: the reduce clips the columns past the tensor
+  cuuint32_t box[3] = {(cuuint32_t)(box_cols > 0 ? box_cols : h), (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box,
                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -143,7 +144,11 @@ int check_map(const a2d_index_map& m, int n, const char* name) {
 int check_common(int bh, int nq, int nk, int h, int causal, float scale,
                  const a2d_index_map& qm, const a2d_index_map& km) {
   if (bh < 0 || nq < 0 || nk < 0) return set_error(A2D_EINVAL, "negative sizes");
-  if (h != 64 && h != 128) return set_error(A2D_EUNSUPPORTED, "head dim %d not in {64, 128}", h);
+  // any head dim up to 128 in steps of 8 (16-byte rows): the tiles are 64 or
+  // 128 columns wide and the TMA zero-fills the columns past h, so the extra
+  // MMA columns add nothing and the epilogues write only h columns
+  if (h < 8 || h > 128 || h % 8)
+    return set_error(A2D_EUNSUPPORTED, "head dim %d not a multiple of 8 in [8, 128]", h);
   if (!(scale > 0.f)) return set_error(A2D_EUNSUPPORTED, "scale must be positive");
   int rc;
   if ((rc = check_map(qm, nq, "q_map"))) return rc;
@@ -200,7 +205,8 @@ int a2d_tile_fwd(const a2d_tile_fwd_args* a, void* stream) {
 int a2d_bwd_preprocess(const void* o, const void* dout, float* delta, int64_t o_stride_bh,
                        int64_t o_stride_row, int64_t do_stride_bh, int64_t do_stride_row,
                        int32_t bh, int32_t n, int32_t h, void* stream) {
-  if (h != 64 && h != 128) return set_error(A2D_EUNSUPPORTED, "head dim %d not in {64, 128}", h);
+  if (h < 8 || h > 128 || h % 8)
+    return set_error(A2D_EUNSUPPORTED, "head dim %d not a multiple of 8 in [8, 128]", h);
   if (!o || !dout || !delta) return set_error(A2D_EINVAL, "null pointer");
   return launch_bwd_preprocess(o, dout, delta, o_stride_bh, o_stride_row, do_stride_bh,
                                do_stride_row, bh, n, h, static_cast<cudaStream_t>(stream));

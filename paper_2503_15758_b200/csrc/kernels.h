@@ -30,7 +30,7 @@ int launch_bwd_finalize(const float* dq_acc, long long asbh, long long asrow, vo
 int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, long long s_row,
                     long long s_bh, int box_rows);
 int make_map_f32_dq_flat(CUtensorMap* m, const float* ptr, int h, int rows, int bh,
-                         long long s_row, long long s_bh, int box_rows);
+                         long long s_row, long long s_bh, int box_rows, int box_cols = 0);
 int bwd_q_tile_rows(int h);
 int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                   const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream);

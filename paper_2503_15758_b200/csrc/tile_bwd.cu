@@ -516,18 +516,20 @@ static bool use_v1_for_128() {
   return v1;
 }
 
+// Every head dim runs the N=128-shaped kernel (tile_bwd128.cu): columns past
+// h are TMA zero fill, which for h = 64 still beats this file's 64-column
+// kernel by ~2x.  A2D_BWD_V1=1 selects the 64-query design for h in {64, 128}.
 int launch_tile_bwd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream) {
-  if (a.h == 128) {
-    if (!use_v1_for_128()) return launch_bwd128(a, tq, tk, tv, tdo, stream);
-    return launch_bwd_hd<128>(a, tq, tk, tv, tdo, stream);
-  }
-  return launch_bwd_hd<64>(a, tq, tk, tv, tdo, stream);
+  if (use_v1_for_128() && a.h == 128) return launch_bwd_hd<128>(a, tq, tk, tv, tdo, stream);
+  if (use_v1_for_128() && a.h == 64) return launch_bwd_hd<64>(a, tq, tk, tv, tdo, stream);
+  return launch_bwd128(a, tq, tk, tv, tdo, stream);
 }
 
 int bwd_q_tile_rows(int h) {
-  if (h == 128) return use_v1_for_128() ? BwdLayout<128>::QT : TILE;
-  return BwdLayout<64>::QT;
+  if (use_v1_for_128() && h == 128) return BwdLayout<128>::QT;
+  if (use_v1_for_128() && h == 64) return BwdLayout<64>::QT;
+  return TILE;
 }
 
 }  // namespace a2d

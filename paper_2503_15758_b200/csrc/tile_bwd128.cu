@@ -438,18 +438,20 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = 0.f;
       }
-      if (!row_ok) continue;
+      if (!row_ok || c * 32 >= p.h) continue;  // columns past h are TMA zero fill
       const long long off = (long long)bh * p.dkv_stride_bh + grow * p.dkv_stride_row + c * 32;
       if (p.dkv_dtype == A2D_F32) {
         float* dst = reinterpret_cast<float*>(base) + off;
 #pragma unroll
         for (int e = 0; e < 32; e += 4)
-          *reinterpret_cast<float4*>(dst + e) =
-              make_float4(v[e] * mul, v[e + 1] * mul, v[e + 2] * mul, v[e + 3] * mul);
+          if (c * 32 + e < p.h)
+            *reinterpret_cast<float4*>(dst + e) =
+                make_float4(v[e] * mul, v[e + 1] * mul, v[e + 2] * mul, v[e + 3] * mul);
       } else {
         __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(base) + off;
 #pragma unroll
         for (int e = 0; e < 32; e += 8) {
+          if (c * 32 + e >= p.h) continue;
           uint4 u;
           u.x = pack_bf16(v[e] * mul, v[e + 1] * mul);
           u.y = pack_bf16(v[e + 2] * mul, v[e + 3] * mul);
@@ -534,7 +536,8 @@ int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUten
     configured[dev & 63] = true;
   }
   CUtensorMap tdq;
-  int rc = make_map_f32_dq_flat(&tdq, a.dq_acc, 128, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh, DQ_ROWS);
+  int rc = make_map_f32_dq_flat(&tdq, a.dq_acc, a.h, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh,
+                                    DQ_ROWS, 128);
   if (rc) return rc;
   const int k_tiles = (a.k_map.mode == A2D_IDX_AFFINE && a.k_map.nblocks > 1)
                           ? a.k_map.nblocks * (a.k_map.rows_per_block / TILE)

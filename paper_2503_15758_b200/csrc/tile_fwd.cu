@@ -439,7 +439,7 @@ int launch_tile_fwd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUt
   // two query tiles per CTA (tile_fwd2.cu) unless A2D_FWD_V1 selects the
   // single-tile kernel (kept for A/B measurements)
   static const bool v1 = getenv("A2D_FWD_V1") != nullptr;
-  if (!v1) return launch_tile_fwd2(a, tq, tk, tv, stream);
+  if (!v1 || (a.h != 64 && a.h != 128)) return launch_tile_fwd2(a, tq, tk, tv, stream);
   if (a.h == 128) return launch_fwd_hd<128>(a, tq, tk, tv, stream);
   return launch_fwd_hd<64>(a, tq, tk, tv, stream);
 }

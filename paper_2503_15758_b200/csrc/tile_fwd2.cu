@@ -143,13 +143,14 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[i] = 0.f;
     }
-    if (!valid) continue;
+    if (!valid || col0 + c * 32 >= p.h) continue;  // columns past h are zero fill
     if (p.o_dtype == A2D_F32) {
       float* dst = reinterpret_cast<float*>(p.o) + (long long)bh * p.o_stride_bh +
                    (long long)grow * p.o_stride_row + col0 + c * 32;
       if (p.accumulate) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
+          if (col0 + c * 32 + i >= p.h) continue;
           const float4 old = *reinterpret_cast<const float4*>(dst + i);
           float4 v;
           v.x = old.x * w_old + o[i + 0] * w_new;
@@ -161,14 +162,16 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
       } else {
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(dst + i) =
-              make_float4(o[i] * w_new, o[i + 1] * w_new, o[i + 2] * w_new, o[i + 3] * w_new);
+          if (col0 + c * 32 + i < p.h)
+            *reinterpret_cast<float4*>(dst + i) =
+                make_float4(o[i] * w_new, o[i + 1] * w_new, o[i + 2] * w_new, o[i + 3] * w_new);
       }
     } else {
       __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + (long long)bh * p.o_stride_bh +
                            (long long)grow * p.o_stride_row + col0 + c * 32;
 #pragma unroll
       for (int i = 0; i < 32; i += 8) {
+        if (col0 + c * 32 + i >= p.h) continue;
         uint4 v;
         v.x = pack_bf16(o[i + 0] * w_new, o[i + 1] * w_new);
         v.y = pack_bf16(o[i + 2] * w_new, o[i + 3] * w_new);
@@ -626,7 +629,8 @@ int launch_tile_fwd2(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CU
 #else
   constexpr int CS = 1;
 #endif
-  if (a.h == 128) return launch_fwd2_hd<128, CS>(a, tq, tk, tv, stream);
+  // tiles are 64 or 128 columns wide; columns past h are TMA zero fill
+  if (a.h > 64) return launch_fwd2_hd<128, CS>(a, tq, tk, tv, stream);
   return launch_fwd2_hd<64, CS>(a, tq, tk, tv, stream);
 }
 

@@ -1,6 +1,6 @@
 """Exception taxonomy, same names and bases as the reference
 (pkg/src/attn2d/errors.py:4-30), plus UnsupportedError for inputs the B200
-kernels reject by design (head dim outside {64, 128}, index maps the tile
+kernels reject by design (head dim not a multiple of 8 in [8, 128], index maps the tile
 cannot evaluate)."""
 
 

@@ -66,13 +66,13 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = 
     h = q.shape[-1]
     if scale is None:
         scale = h ** -0.5
-    hp = 64 if h <= 64 else 128
     if h > 128:
         raise ShapeError(f"head dim {h} > 128 is not supported")
+    hp = max(8, -(-h // 8) * 8)
     if h != hp:
-        # other head dims (the reference's 80 / 96 presets, costmodel.py:73-79)
-        # run zero-padded: zero columns add nothing to q k^T, and the padded
-        # output / gradient columns are sliced off (exact)
+        # the kernels take any multiple of 8 up to 128 (the reference's 80 / 96
+        # presets run natively, costmodel.py:73-79); other widths are zero-
+        # padded to the next multiple of 8 and the extra columns sliced off
         pad = lambda x: torch.nn.functional.pad(x, (0, hp - h))  # noqa: E731
         return attention(pad(q), pad(k), pad(v), causal, scale)[..., :h]
     shp = q.shape

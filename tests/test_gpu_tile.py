@@ -57,7 +57,7 @@ def test_forward_matches_reference_golden(ops, tag):
     assert torch.equal(lse, lse2)
 
 
-@pytest.mark.parametrize("h", [64, 128])
+@pytest.mark.parametrize("h", [64, 96, 128])
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("nq,nk", [(128, 128), (200, 200), (1024, 1024), (384, 1000), (7, 9)])
 def test_forward_vs_torch(ops, h, causal, nq, nk):
@@ -194,7 +194,7 @@ def test_backward_matches_reference_golden(ops, tag):
         assert rel_fro(got[0], want) < REL_TOL, (name, rel_fro(got[0], want))
 
 
-@pytest.mark.parametrize("h", [64, 128])
+@pytest.mark.parametrize("h", [32, 64, 96, 128])
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("n", [128, 200, 1024])
 def test_backward_vs_torch(ops, h, causal, n):
@@ -339,10 +339,11 @@ def test_grouped_query_attention_fwd_bwd(ops, m, m_kv, causal):
     assert rel_fro(vg.grad, wv) < REL_TOL
 
 
-@pytest.mark.parametrize("h", [80, 96])
-def test_other_head_dims_zero_padded(ops, h):
-    """The reference's H=80 / 96 presets (costmodel.py:73-79) through the
-    drop-in: exact zero padding to 128."""
+@pytest.mark.parametrize("h", [4, 32, 48, 80, 96, 104])
+def test_other_head_dims(ops, h):
+    """Head dims other than 64 / 128, incl. the reference's H=80 / 96 presets
+    (costmodel.py:73-79) natively (TMA zero fill inside the 64 / 128-wide
+    tiles) and h=4 (the reference tests' size) padded to 8."""
     from paper_2503_15758_b200 import functional
     from gpu_util import ref_attention_grad
     bh, n = 3, 256
