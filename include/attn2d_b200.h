@@ -18,7 +18,8 @@
  *   - calls are stream-ordered and asynchronous on `stream`;
  *   - no C++ exceptions cross the boundary; return codes:
  *       A2D_OK = 0, A2D_EINVAL = 1 (bad argument / shape),
- *       A2D_EUNSUPPORTED = 2 (valid but unsupported: head dim, index map),
+ *       A2D_EUNSUPPORTED = 2 (valid but unsupported: head dim not a multiple
+ *       of 8 in [8, 128], index map),
  *       A2D_ECUDA = 3 (CUDA launch / runtime error).
  *     a2d_last_error() returns a thread-local message for the last failure.
  *   - tensors are [bh, rows, h] with unit stride along h; strides in elements.
