@@ -353,7 +353,7 @@ def run_ours(args, rank, world, local_rank):
                 out = attention2d(qd, kd, vd, plan)
             out.backward(dod)
             # <O, dO> (the linearised loss whose gradient is dO), one fp32-accumulated dot
-            loss = torch.dot(out.reshape(-1), dod.reshape(-1)).float()
+            loss = torch.dot(out.detach().reshape(-1), dod.reshape(-1)).float()
             res.copy_(loss.reshape(1), non_blocking=True)
             done[s_].record(stream)
 
