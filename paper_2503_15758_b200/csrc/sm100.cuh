@@ -169,6 +169,14 @@ A2D_DEV void tma_load_3d_hint(uint32_t dst, const void* map, uint32_t bar, int c
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+// Plain (non-tensor) bulk reduce-add of `bytes` contiguous fp32 from shared
+// to global memory, bulk-group completion.
+A2D_DEV void bulk_reduce_add_f32(float* gdst, uint32_t src, uint32_t bytes) {
+  asm volatile(
+      "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
+      "r"(src), "r"(bytes)
+      : "memory");
+}
 A2D_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 A2D_DEV void bulk_wait_group_read() {

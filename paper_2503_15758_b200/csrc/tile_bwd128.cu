@@ -466,6 +466,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ------------------------------------------------------------ dQ drain
     const int quarter = warp & 3;
     const int h = quarter * 32 + lane;  // TMEM lane = head dim of dQ^T
+#ifdef B2X_DQ_BULK
+    const bool dq_flat = p.h == 128 && p.dq_stride_row == 128 && p.q_map.nblocks == 1;
+#endif
     const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
     int round = 0;
     TileCursor cur;
@@ -504,6 +507,16 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
 #ifdef B2X_DQ_EVICT_LAST
           tma_reduce_add_3d_g_hint(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh, l2_policy_evict_last());
+#elif defined(B2X_DQ_BULK)
+          if (dq_flat) {  // contiguous rows: one plain bulk reduce per round
+            const int r0 = qrow + DQ_ROWS * r;
+            const int nr = min(DQ_ROWS, p.nq - r0);
+            if (nr > 0)
+              bulk_reduce_add_f32(p.dq_acc + (long long)bh * p.dq_stride_bh + (long long)r0 * 128,
+                                  buf, uint32_t(nr) * 512u);
+          } else {
+            tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);
+          }
 #else
           tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);
 #endif

@@ -1,0 +1,4 @@
+A2D_LIB_PATH=xlib/lib_dqbulk.so timeout 300 python -m pytest tests/test_gpu_tile.py -m gpu -x -q -k backward 2>&1 | tail -1 > gpurun_out/x47.txt
+for r in 1 2; do
+bash tools/run_ab.sh x47 "dqbulk" "bwd 32768 32 128 1" "bwd 131072 32 128 1"
+done
