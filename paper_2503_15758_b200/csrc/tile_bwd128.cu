@@ -203,8 +203,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       // registers; one elected lane issues (the single-lane version issued
       // one MMA per ~70 cycles, slower than the 64-cycle N=128 MMA itself)
       if (n_tiles > 0) {
+        // h < 128: ceil(h/16) K steps for K Q^T / V dO^T and N = 16 ceil(h/16)
+        // for dV / dK (the tiles' other head columns are zero fill)
+        const int ksteps = (p.h + 15) / 16;
         constexpr uint32_t id_ss = make_idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
-        constexpr uint32_t id_kmn = make_idesc_bf16(128, 128, 0, 1);  // P^T dO, dS^T Q
+        const uint32_t id_kmn = make_idesc_bf16(128, ksteps * 16, 0, 1);  // P^T dO, dS^T Q
         constexpr uint32_t id_mnmn = make_idesc_bf16(128, 128, 1, 1); // K^T dS^T
         // K-major SW128: +32 B per K16 step inside a slab, +SLAB per 64 columns;
         // MN-major SW128: +2048 B per K16 step (16 rows of 128 B)
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-              umma_bf16(tmem + col, a + kofs(kk), b + kofs(kk), id_ss, kk > 0);
+              if (kk < ksteps) umma_bf16(tmem + col, a + kofs(kk), b + kofs(kk), id_ss, kk > 0);
           }
           __syncwarp();
         };

@@ -292,8 +292,11 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
       }
     } else if (warp == 1 && n_tiles > 0) {
       // -------------------------------------------------------- MMA issuer (whole warp, one elected lane issues)
+      // head dims below the tile width: only ceil(h/16) K steps for Q K^T and
+      // an N = 16 ceil(h/16) PV (the tile's other columns are zero fill)
+      const int ksteps = (p.h + 15) / 16;
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idesc_pv = make_idesc_bf16(128, HD, 0, 1);
+      const uint32_t idesc_pv = make_idesc_bf16(128, ksteps * 16, 0, 1);
       int ks = 0, kph = 0, vs = 0, vph = 0;
       F2_WAIT(bar(L::B_Q), 0);
       // Descriptors are built once; per MMA only a constant is added to the
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
             const uint64_t off = uint64_t(((kk >> 2) * L::SLAB + (kk & 3) * 32) >> 4);
-            umma_bf16(d, dq + off, dk + off, idesc_qk, kk > 0);
+            if (kk < ksteps) umma_bf16(d, dq + off, dk + off, idesc_qk, kk > 0);
           }
           umma_commit(bar(L::B_SFULL + t));
         }
