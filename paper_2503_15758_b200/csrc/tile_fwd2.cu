@@ -185,7 +185,7 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
 
 template <int CS>
 struct F2Threads {
-  static constexpr int N = 128 + 256 * CS;
+  static constexpr int N = 384;  // producer/MMA warpgroup + 8 softmax warps (both modes)
 };
 
 template <int HD, int CS>
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
   const int rot = pair;  // rotated key sweep
 
   if (warp < 4) {
-    if constexpr (CS == 1) regs_dec<96>(); else regs_dec<32>();
+    regs_dec<96>();
     if (warp == 0 && lane == 0 && n_tiles > 0) {
       // -------------------------------------------------------- producer
       mbar_expect_tx(bar(L::B_Q), 2 * L::TILE_BYTES);
@@ -378,217 +378,225 @@ __global__ void __launch_bounds__(F2Threads<CS>::N, 1)
       }
     }
   } else {
-    if constexpr (CS == 1) regs_inc<200>(); else regs_inc<112>();
-    // ------------------------------------------------------------ softmax WGs
-    constexpr int NC = TILE / CS;  // key columns of S per thread
+    regs_inc<200>();
+    // ------------------------------------------------------------ softmax warps
+    // CS = 1: warp w owns query tile t = (w-4)/4, all 128 key columns.
+    // CS = 2: warp w owns column half h = (w-4)/4 of BOTH tiles (64 columns
+    //         each), so every tile's exponentials run on two warps per SM
+    //         sub-partition; the two halves of a row agree on the running max
+    //         through shared memory and on the overflow re-base through
+    //         barrier.red.or (named barrier 1 + quarter).
+    constexpr int NC = TILE / CS;        // key columns of S per thread and tile
+    constexpr int U = CS;                // tiles served by this warp
     const int sidx = warp - 4;
-    const int t = sidx / (4 * CS);  // query tile of this warpgroup
-    const int h = (sidx >> 2) % CS;  // column half
     const int quarter = warp & 3;
+    const int h = CS == 1 ? 0 : (sidx >> 2);  // column half
     const int row = quarter * 32 + lane;
     const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr + t * 128 + h * NC;
-    const uint32_t p_addr = tmem + lane_addr + t * 128 + h * (NC / 2);
-    const uint32_t o_addr = tmem + lane_addr + (t ? TM_O1 : TM_O0) + h * (HD / CS);
-    float* xch = reinterpret_cast<float*>(smem + L::OFF_XCH) + t * 256;
-    const uint32_t xbar = 1 + t * 4 + quarter;  // named barrier of this row quarter's halves
-    const bool present = (t == 0) || has1;
-    const TileRef qt = t ? qt1 : qt0;
+    const uint32_t xbar = 1 + quarter;
     const float sl2 = p.scale * kLog2e;
-    float m_run = -INFINITY;  // running max of scale*log2e*s (common to both halves)
-    float l_run = 0.f;        // this half's share of the denominator
-    // Per-tile mask classes for affine maps are computed 32 tiles at a time,
-    // one tile per lane, and broadcast with one shuffle per tile: the sweep
-    // itself carries no index arithmetic.  Explicit index arrays keep the
-    // per-tile binary-search path.
     const bool arr = p.q_map.mode == A2D_IDX_ARRAY;
     const int rot0 = n_tiles > 0 ? rot % n_tiles : 0;
-    uint32_t my_info = 0;
-    TileCursor cur;
-    if (arr) cur.start(kr, rot);
+    float m_run[U], l_run[U];
+    uint32_t my_info[U];
+    TileCursor cur[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      m_run[u] = -INFINITY;  // running max of scale*log2e*s (common to both halves)
+      l_run[u] = 0.f;        // this half's share of the denominator
+      my_info[u] = 0;
+      if (arr) cur[u].start(kr, rot);
+    }
     for (int j = 0; j < n_tiles; ++j) {
-      bool partial;
-      int lim = TILE - 1;  // last visible key column of this row (tile-relative)
-      if (!present) {
-        partial = true;
-        lim = -1;
-      } else if (arr) {
-        const TileRef kt = tile_ref(p.k_map, p.nk, cur.row0(p.k_map));
-        cur.next(kr);
-        const PairMask pm = pair_mask(p.q_map, qt, kt, causal);
-        partial = pm.partial;
-        if (partial) lim = row_limit(p.q_map, p.k_map, qt, kt, pm, causal, row);
-      } else {
-        if ((j & 31) == 0) {
-          const int f = j + lane;
-          my_info = 0;
-          if (f < n_tiles) {
-            const int g = rot0 + f < n_tiles ? rot0 + f : rot0 + f - n_tiles;
-            const TileRef kt = tile_ref(p.k_map, p.nk, range_row0(kr, p.k_map, g));
-            const PairMask q = pair_mask(p.q_map, qt, kt, causal);
-            my_info = uint32_t(q.thr + 512) | (uint32_t(q.kvalid) << 16) |
-                      (q.partial ? 0x80000000u : 0u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = CS == 1 ? (sidx >> 2) : u;  // query tile of this unit
+        const uint32_t s_addr = tmem + lane_addr + t * 128 + h * NC;
+        const uint32_t p_addr = tmem + lane_addr + t * 128 + h * (NC / 2);
+        const uint32_t o_addr = tmem + lane_addr + (t ? TM_O1 : TM_O0) + h * (HD / CS);
+        float* xch = reinterpret_cast<float*>(smem + L::OFF_XCH) + t * 256;
+        const bool present = (t == 0) || has1;
+        const TileRef qt = t ? qt1 : qt0;
+        // Per-tile mask classes for affine maps are computed 32 tiles at a
+        // time, one tile per lane, and broadcast with one shuffle per tile;
+        // explicit index arrays keep the per-tile binary-search path.
+        bool partial;
+        int lim = TILE - 1;  // last visible key column of this row (tile-relative)
+        if (!present) {
+          partial = true;
+          lim = -1;
+        } else if (arr) {
+          const TileRef kt = tile_ref(p.k_map, p.nk, cur[u].row0(p.k_map));
+          cur[u].next(kr);
+          const PairMask pm = pair_mask(p.q_map, qt, kt, causal);
+          partial = pm.partial;
+          if (partial) lim = row_limit(p.q_map, p.k_map, qt, kt, pm, causal, row);
+        } else {
+          if ((j & 31) == 0) {
+            const int f = j + lane;
+            my_info[u] = 0;
+            if (f < n_tiles) {
+              const int g = rot0 + f < n_tiles ? rot0 + f : rot0 + f - n_tiles;
+              const TileRef kt = tile_ref(p.k_map, p.nk, range_row0(kr, p.k_map, g));
+              const PairMask q = pair_mask(p.q_map, qt, kt, causal);
+              my_info[u] = uint32_t(q.thr + 512) | (uint32_t(q.kvalid) << 16) |
+                           (q.partial ? 0x80000000u : 0u);
+            }
+          }
+          const uint32_t inf = __shfl_sync(0xffffffffu, my_info[u], j & 31);
+          partial = (inf >> 31) != 0;
+          if (partial) {
+            const int kvalid = int((inf >> 16) & 0xff);
+            lim = causal ? min(row - (int(inf & 0xffff) - 512), kvalid - 1) : kvalid - 1;
           }
         }
-        const uint32_t inf = __shfl_sync(0xffffffffu, my_info, j & 31);
-        partial = (inf >> 31) != 0;
-        if (partial) {
-          const int kvalid = int((inf >> 16) & 0xff);
-          lim = causal ? min(row - (int(inf & 0xffff) - 512), kvalid - 1) : kvalid - 1;
-        }
-      }
-      lim -= h * NC;  // relative to this half's first column
-      mbar_wait(bar(L::B_SFULL + t), j & 1);
-      tc_fence_after();
-      TR(0 * 8 + t * 4 + quarter, j);
+        lim -= h * NC;  // relative to this half's first column
+        mbar_wait(bar(L::B_SFULL + t), j & 1);
+        tc_fence_after();
+        TR(0 * 8 + t * 4 + quarter, j);
 #ifdef F2X_NOSOFTMAX
-      if (true) {
-        tc_fence_before();
-        mbar_arrive(bar(L::B_PFULL + t));
-        continue;
-      }
+        if (true) {
+          tc_fence_before();
+          mbar_arrive(bar(L::B_PFULL + t));
+          continue;
+        }
 #endif
-      float s[NC];
-      auto load_s = [&]() {  // S_t(j) row from TMEM, causal / ragged columns masked
+        float s[NC];
+        auto load_s = [&]() {  // S_t(j) row from TMEM, causal / ragged columns masked
 #pragma unroll
-        for (int c = 0; c < NC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
-        tmem_wait_ld();
-        if (partial) {
-#pragma unroll
-          for (int jj = 0; jj < NC; ++jj)
-            if (jj > lim) s[jj] = -INFINITY;
-        }
-      };
-      load_s();
-      TR(1 * 8 + t * 4 + quarter, j);
-      float alpha = 1.f;
-      uint32_t pk[NC / 2];
-      const float2 sc = make_float2(sl2, sl2);
-      // exponentials of this tile against the running max (P in pk, returns
-      // the tile's share of the denominator)
-      auto exps = [&](float mbase) -> float {
-        float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-        const float2 nb = make_float2(-mbase, -mbase);
-        if (partial) {  // masked entries are -inf: the exact MUFU path keeps them 0
-#pragma unroll
-          for (int jj = 0; jj < NC; jj += 2) {
-            const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
-            const float2 e = make_float2(XEX2(x.x), XEX2(x.y));
-            acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
-            pk[jj / 2] = pack_bf16(e.x, e.y);
-          }
-        } else {  // some exponentials on the FMA pipe (MUFU offload, F2_POLY)
-#pragma unroll
-          for (int jj = 0; jj < NC; jj += 2) {
-            const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
-            float2 e;
-            if (F2_POLY(jj)) e = exp2_poly2(x);
-            else e = make_float2(XEX2(x.x), XEX2(x.y));
-            acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
-            pk[jj / 2] = pack_bf16(e.x, e.y);
-          }
-        }
-        const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-        const float2 a = fadd2(a01, a23);
-        return a.x + a.y;
-      };
-      auto move_max = [&]() {  // exact running max of this tile (log2 domain)
-        float mx = rowmax<NC>(s) * sl2;
-        if constexpr (CS == 2) {
-          // both halves of a row need one common max: exchange through smem.
-          // One slot per (tile, half, row) suffices: the partner reads it
-          // before arriving on PFULL(j), and this slot is rewritten only after
-          // S(j+1), i.e. after PV(j) consumed both halves' P.
-          xch[h * 128 + row] = mx;
-          named_bar_sync(xbar, 64);
-          mx = fmaxf(mx, xch[(h ^ 1) * 128 + row]);
-        }
-        return mx;
-      };
-#ifdef F2X_ROWMAX
-      {  // classic: row max every tile, moved when it grows by > 2^8
-        const float m_new = fmaxf(m_run, move_max());
-        if (m_new > m_run + kRescaleThreshold) {
-          alpha = ex2(m_run - m_new);
-          m_run = m_new;
-        }
-      }
-      float tsum = exps(m_run == -INFINITY ? 0.f : m_run);
-#else
-      // No row max in the steady state: P = 2^(x - m_run) with the max of the
-      // row's first visible tile.  Values above 1 are exact in bf16 / fp32
-      // (relative precision), so the max only has to move when a tile's sum
-      // nears overflow (>= 2^64, or non-finite) — then it is recomputed
-      // exactly and the tile redone.  Saves the 128-wide max tree per tile.
-      // (m_run is identical in both column halves of a row, so with CS == 2
-      // both warps take this branch together and meet in move_max's barrier)
-      if (__any_sync(0xffffffffu, m_run == -INFINITY)) {
-        const float m_new = fmaxf(m_run, move_max());
-        if (m_new > m_run) {
-          alpha = (m_run == -INFINITY) ? 1.f : ex2(m_run - m_new);
-          m_run = m_new;
-        }
-      }
-      TR(2 * 8 + t * 4 + quarter, j);
-      float tsum = exps(m_run == -INFINITY ? 0.f : m_run);
-      bool ovf = __any_sync(0xffffffffu, !(tsum < 0x1p64f));
-      if constexpr (CS == 2) ovf = bar_red_or(xbar, 64, ovf);  // one decision for both halves
-      if (ovf) {  // rare: S is still in TMEM
-        load_s();
-        const float m_new = fmaxf(m_run, move_max());
-        if (m_new > m_run) {
-          alpha *= (m_run == -INFINITY) ? 1.f : ex2(m_run - m_new);
-          m_run = m_new;
-        }
-        tsum = exps(m_run == -INFINITY ? 0.f : m_run);
-      }
-#endif
-      l_run = l_run * alpha + tsum;
-#ifndef F2X_ROWMAX
-      if (l_run > 0x1p96f) {  // keep the denominator far from fp32 overflow
-        l_run *= 0x1p-64f;
-        alpha *= 0x1p-64f;
-        m_run += 64.f;
-      }
-#endif
-      TR(3 * 8 + t * 4 + quarter, j);
-      // P_t(j), this half's keys, over S_t columns that are already consumed
-      // (half 1 writes columns 32..63 of S, which half 0 loaded before the
-      // exchange barrier)
-#pragma unroll
-      for (int c = 0; c < NC / 64; ++c)
-        tmem_st32(p_addr + c * 32, reinterpret_cast<const float*>(pk + c * 32));
-      // O_t already holds PV_t(j-1) (its commit preceded S_t(j)'s): rescale
-      // this half's columns in place when the running max moved
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-        for (int c = 0; c < HD / CS / 32; ++c) {
-          float o[32];
-          tmem_ld32(o_addr + c * 32, o);
+          for (int c = 0; c < NC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
           tmem_wait_ld();
+          if (partial) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] *= alpha;
-          tmem_st32(o_addr + c * 32, o);
+            for (int jj = 0; jj < NC; ++jj)
+              if (jj > lim) s[jj] = -INFINITY;
+          }
+        };
+        load_s();
+        TR(1 * 8 + t * 4 + quarter, j);
+        float alpha = 1.f;
+        uint32_t pk[NC / 2];
+        const float2 sc = make_float2(sl2, sl2);
+        // exponentials of this tile against the running max (P in pk, returns
+        // the tile's share of the denominator)
+        auto exps = [&](float mbase) -> float {
+          float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+          const float2 nb = make_float2(-mbase, -mbase);
+          if (partial) {  // masked entries are -inf: the exact MUFU path keeps them 0
+#pragma unroll
+            for (int jj = 0; jj < NC; jj += 2) {
+              const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
+              const float2 e = make_float2(XEX2(x.x), XEX2(x.y));
+              acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
+              pk[jj / 2] = pack_bf16(e.x, e.y);
+            }
+          } else {  // some exponentials on the FMA pipe (MUFU offload, F2_POLY)
+#pragma unroll
+            for (int jj = 0; jj < NC; jj += 2) {
+              const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
+              float2 e;
+              if (F2_POLY(jj)) e = exp2_poly2(x);
+              else e = make_float2(XEX2(x.x), XEX2(x.y));
+              acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
+              pk[jj / 2] = pack_bf16(e.x, e.y);
+            }
+          }
+          const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+          const float2 a = fadd2(a01, a23);
+          return a.x + a.y;
+        };
+        auto move_max = [&]() {  // exact running max of this tile (log2 domain)
+          float mx = rowmax<NC>(s) * sl2;
+          if constexpr (CS == 2) {
+            // both halves of a row need one common max: exchange through smem
+            // (slot (tile, half, row); the partner reads it before arriving on
+            // PFULL(j) and it is rewritten only after S(j+1) is full)
+            xch[h * 128 + row] = mx;
+            named_bar_sync(xbar, 64);
+            mx = fmaxf(mx, xch[(h ^ 1) * 128 + row]);
+          }
+          return mx;
+        };
+        // No row max in the steady state: P = 2^(x - m_run) with the max of the
+        // row's first visible tile.  Values above 1 are exact in bf16 / fp32
+        // (relative precision), so the max only has to move when a tile's sum
+        // nears overflow (>= 2^64, or non-finite) — then it is recomputed
+        // exactly and the tile redone.  (m_run is identical in both halves of
+        // a row, so both warps of a pair take these branches together.)
+        if (__any_sync(0xffffffffu, m_run[u] == -INFINITY)) {
+          const float m_new = fmaxf(m_run[u], move_max());
+          if (m_new > m_run[u]) {
+            alpha = (m_run[u] == -INFINITY) ? 1.f : ex2(m_run[u] - m_new);
+            m_run[u] = m_new;
+          }
         }
+        TR(2 * 8 + t * 4 + quarter, j);
+        float tsum = exps(m_run[u] == -INFINITY ? 0.f : m_run[u]);
+        bool ovf = __any_sync(0xffffffffu, !(tsum < 0x1p64f));
+        if constexpr (CS == 2) ovf = bar_red_or(xbar, 64, ovf);  // one decision for both halves
+        if (ovf) {  // rare: S is still in TMEM
+          load_s();
+          const float m_new = fmaxf(m_run[u], move_max());
+          if (m_new > m_run[u]) {
+            alpha *= (m_run[u] == -INFINITY) ? 1.f : ex2(m_run[u] - m_new);
+            m_run[u] = m_new;
+          }
+          tsum = exps(m_run[u] == -INFINITY ? 0.f : m_run[u]);
+        }
+        l_run[u] = l_run[u] * alpha + tsum;
+        if (l_run[u] > 0x1p96f) {  // keep the denominator far from fp32 overflow
+          l_run[u] *= 0x1p-64f;
+          alpha *= 0x1p-64f;
+          m_run[u] += 64.f;
+        }
+        TR(3 * 8 + t * 4 + quarter, j);
+        // P_t(j), this half's keys, over S_t columns already consumed (half 1
+        // writes columns 32..63 of S, which half 0 loaded before it could
+        // reach the P store: both halves passed this tile's barrier.red)
+#pragma unroll
+        for (int c = 0; c < NC / 64; ++c)
+          tmem_st32(p_addr + c * 32, reinterpret_cast<const float*>(pk + c * 32));
+        // O_t already holds PV_t(j-1) (its commit preceded S_t(j)'s): rescale
+        // this half's columns in place when the running max moved
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < HD / CS / 32; ++c) {
+            float o[32];
+            tmem_ld32(o_addr + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            tmem_st32(o_addr + c * 32, o);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        TR(4 * 8 + t * 4 + quarter, j);
+        mbar_arrive(bar(L::B_PFULL + t));
       }
-      tmem_wait_st();
-      tc_fence_before();
-      TR(4 * 8 + t * 4 + quarter, j);
-      mbar_arrive(bar(L::B_PFULL + t));
     }
     // ------------------------------------------------------------ epilogue
-    if (n_tiles > 0) {
-      mbar_wait(bar(L::B_ODONE + t), 0);
-      tc_fence_after();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = CS == 1 ? (sidx >> 2) : u;
+      const uint32_t o_addr = tmem + lane_addr + (t ? TM_O1 : TM_O0) + h * (HD / CS);
+      float* xch = reinterpret_cast<float*>(smem + L::OFF_XCH) + t * 256;
+      const bool present = (t == 0) || has1;
+      const TileRef qt = t ? qt1 : qt0;
+      if (n_tiles > 0) {
+        mbar_wait(bar(L::B_ODONE + t), 0);
+        tc_fence_after();
+      }
+      float l = l_run[u];
+      if constexpr (CS == 2) {  // the row's denominator is the sum of both halves
+        xch[h * 128 + row] = l;
+        named_bar_sync(xbar, 64);
+        l += xch[(h ^ 1) * 128 + row];
+      }
+      if (present)
+        f2_epilogue<HD, HD / CS>(p, o_addr, n_tiles > 0, bh, qt.row0 + row, row < qt.nvalid,
+                                 m_run[u], l, h * (HD / CS), h == 0);
     }
-    if constexpr (CS == 2) {  // the row's denominator is the sum of both halves
-      xch[h * 128 + row] = l_run;
-      named_bar_sync(xbar, 64);
-      l_run += xch[(h ^ 1) * 128 + row];
-    }
-    if (present)
-      f2_epilogue<HD, HD / CS>(p, o_addr, n_tiles > 0, bh, qt.row0 + row, row < qt.nvalid, m_run,
-                               l_run, h * (HD / CS), h == 0);
   }
 
   tc_fence_before();
