@@ -136,6 +136,68 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int qrot = kt_idx;  // rotated q sweep: co-resident CTAs reduce into different dQ rows
 #endif
 
+  // ---------------------------------------------------------------- MMA issue
+  // Warp-level helpers (one elected lane issues; whole warp converged):
+  // h < 128: ceil(h/16) K steps for K Q^T / V dO^T and N = 16 ceil(h/16)
+  // for dV / dK (the tiles' other head columns are zero fill)
+  const int ksteps = (p.h + 15) / 16;
+  constexpr uint32_t id_ss = make_idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
+  const uint32_t id_kmn = make_idesc_bf16(128, ksteps * 16, 0, 1);  // P^T dO, dS^T Q
+  constexpr uint32_t id_mnmn = make_idesc_bf16(128, 128, 1, 1); // K^T dS^T
+  // K-major SW128: +32 B per K16 step inside a slab, +SLAB per 64 columns;
+  // MN-major SW128: +2048 B per K16 step (16 rows of 128 B)
+  auto kofs = [](int kk) { return uint64_t(((kk >> 2) * SLAB + (kk & 3) * 32) >> 4); };
+  auto mofs = [](int kk) { return uint64_t((kk * 2048) >> 4); };
+  constexpr uint64_t QSTEP = TILE_B >> 4;
+  auto commit = [&](int b) {
+    if (elect_one()) umma_commit(bar(b));
+    __syncwarp();
+  };
+  auto issue_s = [&](uint32_t col, uint64_t a, uint64_t b) {
+    a = opaque64(a);
+    b = opaque64(b);
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        if (kk < ksteps) umma_bf16(tmem + col, a + kofs(kk), b + kofs(kk), id_ss, kk > 0);
+    }
+    __syncwarp();
+  };
+  auto issue_dv = [&](int i) {  // dV += P^T dO_i (P^T in TMEM: WG A's queries at X+0, B's at X+64)
+    if (elect_one()) {
+      const uint64_t dob = opaque64(make_sdesc(sb + OFF_DO, SLAB, 1024));
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        umma_bf16_ts(tmem + TM_DV, tmem + TM_X + (kk >> 2) * 64 + (kk & 3) * 8,
+                     dob + mofs(kk), id_kmn, (i > 0 || kk > 0));
+    }
+    __syncwarp();
+  };
+  // dQ^T = K^T dS^T -> Y, then dK += dS^T Q_i; commits DQFULL, QEMPTY, DSFREE
+  auto issue_dq_dk = [&](int i) {
+    const int qs = i & 1;
+    if (elect_one()) {
+      const uint64_t kb = opaque64(make_sdesc(sb + OFF_K, SLAB, 1024));
+      const uint64_t dsb = opaque64(make_sdesc(sb + OFF_DS, SLAB, 1024));
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        umma_bf16(tmem + TM_Y, kb + mofs(kk), dsb + mofs(kk), id_mnmn, kk > 0);
+      umma_commit(bar(B_DQFULL));
+      const uint64_t dsk = opaque64(make_sdesc(sb + OFF_DS, 16, 1024));
+      const uint64_t qb = opaque64(make_sdesc(sb + OFF_Q, SLAB, 1024) + qs * QSTEP);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        umma_bf16(tmem + TM_DK, dsk + kofs(kk), qb + mofs(kk), id_kmn, (i > 0 || kk > 0));
+      umma_commit(bar(B_QEMPTY0 + qs));
+      umma_commit(bar(B_DSFREE));
+    }
+    __syncwarp();
+  };
+  const uint64_t k_k = make_sdesc(sb + OFF_K, 16, 1024);
+  const uint64_t v_k = make_sdesc(sb + OFF_V, 16, 1024);
+  const uint64_t do_k = make_sdesc(sb + OFF_DO, 16, 1024);
+  const uint64_t q_k = make_sdesc(sb + OFF_Q, 16, 1024);
+
   if (warp < 4) {
     regs_dec<72>();
     if (warp == 0) {
@@ -203,40 +265,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       // registers; one elected lane issues (the single-lane version issued
       // one MMA per ~70 cycles, slower than the 64-cycle N=128 MMA itself)
       if (n_tiles > 0) {
-        // h < 128: ceil(h/16) K steps for K Q^T / V dO^T and N = 16 ceil(h/16)
-        // for dV / dK (the tiles' other head columns are zero fill)
-        const int ksteps = (p.h + 15) / 16;
-        constexpr uint32_t id_ss = make_idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
-        const uint32_t id_kmn = make_idesc_bf16(128, ksteps * 16, 0, 1);  // P^T dO, dS^T Q
-        constexpr uint32_t id_mnmn = make_idesc_bf16(128, 128, 1, 1); // K^T dS^T
-        // K-major SW128: +32 B per K16 step inside a slab, +SLAB per 64 columns;
-        // MN-major SW128: +2048 B per K16 step (16 rows of 128 B)
-        auto kofs = [](int kk) { return uint64_t(((kk >> 2) * SLAB + (kk & 3) * 32) >> 4); };
-        auto mofs = [](int kk) { return uint64_t((kk * 2048) >> 4); };
-        const uint64_t k_k = make_sdesc(sb + OFF_K, 16, 1024);
-        const uint64_t v_k = make_sdesc(sb + OFF_V, 16, 1024);
-        const uint64_t do_k = make_sdesc(sb + OFF_DO, 16, 1024);
-        const uint64_t ds_k = make_sdesc(sb + OFF_DS, 16, 1024);
-        const uint64_t q_k = make_sdesc(sb + OFF_Q, 16, 1024);
-        const uint64_t k_mn = make_sdesc(sb + OFF_K, SLAB, 1024);
-        const uint64_t ds_mn = make_sdesc(sb + OFF_DS, SLAB, 1024);
-        const uint64_t do_mn = make_sdesc(sb + OFF_DO, SLAB, 1024);
-        const uint64_t q_mn = make_sdesc(sb + OFF_Q, SLAB, 1024);
-        constexpr uint64_t QSTEP = TILE_B >> 4;
-        auto commit = [&](int b) {
-          if (elect_one()) umma_commit(bar(b));
-          __syncwarp();
-        };
-        auto issue_s = [&](uint32_t col, uint64_t a, uint64_t b) {
-          a = opaque64(a);
-          b = opaque64(b);
-          if (elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              if (kk < ksteps) umma_bf16(tmem + col, a + kofs(kk), b + kofs(kk), id_ss, kk > 0);
-          }
-          __syncwarp();
-        };
         mbar_wait(bar(B_KV), 0);
         mbar_wait(bar(B_QFULL0), 0);
         tc_fence_after();
@@ -250,17 +278,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc_fence_after();
           issue_s(TM_Y, v_k, do_k);
           commit(B_DPFULL);
-          // dV += P^T dO_i (P^T in TMEM: warpgroup A's 64 queries at X+0, B's at X+64)
           mbar_wait(bar(B_PREADY), i & 1);
           tc_fence_after();
-          if (elect_one()) {
-            const uint64_t dob = opaque64(do_mn);
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_bf16_ts(tmem + TM_DV, tmem + TM_X + (kk >> 2) * 64 + (kk & 3) * 8,
-                           dob + mofs(kk), id_kmn, (i > 0 || kk > 0));
-          }
-          __syncwarp();
+          issue_dv(i);
           commit(B_DOEMPTY);
           // S_{i+1} -> X: dV_i has read P_i out of X (in-order pipe)
           if (i + 1 < n_tiles) {
@@ -273,20 +293,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           // then dK += dS^T Q_i while the drain empties Y
           mbar_wait(bar(B_DSREADY), i & 1);
           tc_fence_after();
-          if (elect_one()) {
-            const uint64_t kb = opaque64(k_mn), dsb = opaque64(ds_mn);
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_bf16(tmem + TM_Y, kb + mofs(kk), dsb + mofs(kk), id_mnmn, kk > 0);
-            umma_commit(bar(B_DQFULL));
-            const uint64_t dsk = opaque64(ds_k), qb = opaque64(q_mn + qs * QSTEP);
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_bf16(tmem + TM_DK, dsk + kofs(kk), qb + mofs(kk), id_kmn, (i > 0 || kk > 0));
-            umma_commit(bar(B_QEMPTY0 + qs));
-            umma_commit(bar(B_DSFREE));
-          }
-          __syncwarp();
+          issue_dq_dk(i);
         }
         commit(B_DONE);
       }
