@@ -129,3 +129,35 @@ def test_error_taxonomy_mapping():
             _lib.check(_lib.A2D_ECUDA, "x")
     finally:
         _lib._LIB = saved
+
+
+def test_no_cpu_fallback():
+    """The product path refuses to run without the CUDA extension or on host
+    tensors: there is no CPU fallback to silently take over."""
+    import torch
+    from paper_2503_15758_b200 import ops
+    with pytest.raises(RuntimeError):
+        _lib.load("/nonexistent/libattn2d_b200.so")
+    q = torch.zeros((1, 128, 64), dtype=torch.bfloat16)
+    with pytest.raises(ShapeError):
+        ops.tile_forward(q, q, q, causal=True, scale=0.125)
+
+
+def test_abi_argument_validation_without_a_gpu():
+    """Invalid calls are rejected by the C ABI before any CUDA work, with the
+    documented return codes (include/attn2d_b200.h)."""
+    lib = _lib.load()
+    a = _lib.TileFwdArgs()
+    a.q = a.k = a.v = a.o = a.lse = 16  # never dereferenced: validation fails first
+    a.bh, a.nq, a.nk, a.causal, a.scale, a.o_dtype = 2, 128, 128, 1, 0.125, _lib.BF16
+    for m in (a.q_map, a.k_map):
+        m.mode, m.nblocks, m.rows_per_block, m.stride = _lib.IDX_AFFINE, 1, 128, 1
+    a.h = 100                                   # not a multiple of 8
+    assert lib.a2d_tile_fwd(a, None) == _lib.A2D_EUNSUPPORTED
+    a.h = 136                                   # wider than the tiles
+    assert lib.a2d_tile_fwd(a, None) == _lib.A2D_EUNSUPPORTED
+    a.h, a.kv_group = 64, 3                     # 3 does not divide bh = 2
+    assert lib.a2d_tile_fwd(a, None) == _lib.A2D_EINVAL
+    a.kv_group, a.nq = 1, -1
+    assert lib.a2d_tile_fwd(a, None) == _lib.A2D_EINVAL
+    assert b"negative" in lib.a2d_last_error()
