@@ -84,7 +84,11 @@ struct F2Layout {
   static constexpr int SLAB = TILE * 128;  // one 128-row x 64-col bf16 slab
   static constexpr int SLABS = HD / 64;
   static constexpr int TILE_BYTES = SLAB * SLABS;
+#ifdef F2X_KST2
+  static constexpr int KST = 2;
+#else
   static constexpr int KST = 3;
+#endif
   static constexpr int VST = HD == 128 ? 2 : 3;
   static constexpr int OFF_Q = 0;  // Q0, Q1
   static constexpr int OFF_K = OFF_Q + 2 * TILE_BYTES;
