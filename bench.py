@@ -348,7 +348,7 @@ def run_ours(args, rank, world, local_rank):
             qd, kd, vd = (t.detach().requires_grad_(True) for t in bufs[s_][:3])
             dod = bufs[s_][3]
             if world == 1:
-                out = functional.attention(qd, kd, vd, causal=True, scale=scale)
+                out = functional.attention(qd, kd, vd, causal=causal, scale=scale)
             else:
                 out = attention2d(qd, kd, vd, plan)
             out.backward(dod)

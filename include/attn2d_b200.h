@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define A2D_ABI_VERSION 2
+#define A2D_ABI_VERSION 3
 #define A2D_MAX_BLOCKS 16
 
 enum { A2D_OK = 0, A2D_EINVAL = 1, A2D_EUNSUPPORTED = 2, A2D_ECUDA = 3 };
@@ -116,7 +116,10 @@ int a2d_bwd_preprocess(const void* o, const void* dout, float* delta,
  *   dq_acc [bh, nq, h] fp32 (strides dq_stride_*, multiples of 4 elements):
  *   dS K (unscaled) is ADDED to it with TMA reduce-add (caller zeroes);
  *   dk, dv [bh, nk, h]: written (dkv_dtype A2D_F32 or A2D_BF16); dk is
- *   already multiplied by scale.
+ *   already multiplied by scale.  accumulate_dkv = 1 ADDS the contributions
+ *   to the fp32 dk / dv already in the buffers instead (the ring's and the
+ *   overlapped schedule's per-hop accumulation, reference ring.py:118-143).
+ *   nq == 0 writes zero dk / dv (nothing attends these keys).
  *   kv_group: as for a2d_tile_fwd (k/v hold bh / kv_group heads); dk / dv
  *   stay per QUERY head, the caller sums each group. */
 typedef struct {
@@ -139,7 +142,7 @@ typedef struct {
   int32_t causal;
   float scale;
   int32_t dkv_dtype;
-  int32_t reserved;
+  int32_t accumulate_dkv;
   a2d_index_map q_map;
   a2d_index_map k_map;
   int32_t kv_group;

@@ -16,7 +16,7 @@ from .errors import ShapeError, UnsupportedError
 
 LIB_PATH = Path(os.environ.get("A2D_LIB_PATH") or
                 Path(__file__).resolve().parent / "libattn2d_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_BLOCKS = 16
 
 A2D_OK, A2D_EINVAL, A2D_EUNSUPPORTED, A2D_ECUDA = 0, 1, 2, 3
@@ -60,7 +60,7 @@ class TileBwdArgs(ctypes.Structure):
                 ("dkv_stride_bh", c_int64), ("dkv_stride_row", c_int64),
                 ("bh", c_int32), ("nq", c_int32), ("nk", c_int32), ("h", c_int32),
                 ("causal", c_int32), ("scale", c_float), ("dkv_dtype", c_int32),
-                ("reserved", c_int32), ("q_map", IndexMap), ("k_map", IndexMap),
+                ("accumulate_dkv", c_int32), ("q_map", IndexMap), ("k_map", IndexMap),
                 ("kv_group", c_int32), ("reserved2", c_int32)]
 
 

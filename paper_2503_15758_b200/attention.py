@@ -219,10 +219,15 @@ def flash_attn_backward(q: TokenShard, k: TokenShard, v: TokenShard, o, d_out, m
         raise ShapeError(f"o/d_out shape {tuple(o.shape)}/{tuple(d_out.shape)} does not match q rows")
     if m.shape != (q.rows,) or d.shape != (q.rows,):
         raise ShapeError("statistics m, d must have one entry per query row")
+    if q.data.shape[1] != k.data.shape[1]:
+        raise ShapeError(f"head dims differ: q {tuple(q.data.shape)} k {tuple(k.data.shape)}")
     if bool((d == 0).any()):
         raise FullyMaskedRowError(
             f"rows {torch.nonzero(d == 0).flatten().tolist()} have empty statistics")
     dev = _device()
+    if q.rows == 0 or k.rows == 0:  # nothing attends: zero gradients (attention.py:250-252)
+        z = lambda r, c: torch.zeros((r, c), dtype=torch.float32, device=dev)  # noqa: E731
+        return z(q.rows, q.data.shape[1]), z(k.rows, k.data.shape[1]), z(v.rows, h)
     hp = _padded_h(max(h, q.data.shape[1]))
     lse = (m.to(dev, torch.float64) + torch.log(d.to(dev, torch.float64))).to(torch.float32)
     qb, kb, vb = _to_bf16(q.data, hp), _to_bf16(k.data, hp), _to_bf16(v.data, hp)
@@ -234,7 +239,8 @@ def flash_attn_backward(q: TokenShard, k: TokenShard, v: TokenShard, o, d_out, m
                                        causal=mask.kind is MaskKind.CAUSAL, scale=float(scale),
                                        q_index=qi, k_index=ki)
     dq = dq_acc * float(scale)
-    return dq[0, :, :h], dk[0, :, :h], dv[0, :, :h]
+    hq = q.data.shape[1]
+    return dq[0, :, :hq], dk[0, :, :hq], dv[0, :, :h]
 
 
 def count_unmasked(q_idx, k_idx, causal: bool) -> int:

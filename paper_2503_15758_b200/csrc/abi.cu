@@ -220,9 +220,24 @@ int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
   if (a->kv_group < 0 || a->bh % g) return set_error(A2D_EINVAL, "kv_group %d must divide bh %d", a->kv_group, a->bh);
   if (a->dkv_dtype != A2D_F32 && a->dkv_dtype != A2D_BF16)
     return set_error(A2D_EINVAL, "dkv_dtype invalid");
-  if (!a->lse || !a->delta || !a->dq_acc || !a->dk || !a->dv)
-    return set_error(A2D_EINVAL, "null output / statistics pointer");
+  if (!a->dk || !a->dv) return set_error(A2D_EINVAL, "null dk / dv pointer");
+  if (a->nq > 0 && (!a->lse || !a->delta || !a->dq_acc))
+    return set_error(A2D_EINVAL, "null dq_acc / statistics pointer");
+  if (a->accumulate_dkv && a->dkv_dtype != A2D_F32)
+    return set_error(A2D_EINVAL, "accumulate_dkv requires fp32 dk / dv");
   if (a->bh == 0 || a->nk == 0) return A2D_OK;
+  if (a->nq == 0) {  // no query rows: zero gradients (reference attention.py:250-252)
+    if (a->accumulate_dkv) return A2D_OK;
+    if ((a->dkv_stride_bh | a->dkv_stride_row) % 4)
+      return set_error(A2D_EINVAL, "dk / dv strides must be multiples of 4 elements");
+    int r = launch_bwd_finalize(nullptr, 0, 0, a->dk, a->dkv_dtype, a->dkv_stride_bh,
+                                a->dkv_stride_row, a->bh, a->nk, a->h, 0.f,
+                                static_cast<cudaStream_t>(stream));
+    if (r) return r;
+    return launch_bwd_finalize(nullptr, 0, 0, a->dv, a->dkv_dtype, a->dkv_stride_bh,
+                               a->dkv_stride_row, a->bh, a->nk, a->h, 0.f,
+                               static_cast<cudaStream_t>(stream));
+  }
   CUtensorMap tq, tk, tv, tdo;
   const int qt = bwd_q_tile_rows(a->h);
   if ((rc = make_map(&tq, a->q, a->h, a->nq, a->bh, a->q_stride_row, a->q_stride_bh, "q", qt))) return rc;

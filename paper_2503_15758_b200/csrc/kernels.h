@@ -13,8 +13,6 @@ int check_launch(const char* what);
 
 int launch_tile_fwd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, cudaStream_t stream);
-int launch_tile_fwd2(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
-                     const CUtensorMap& tv, cudaStream_t stream);
 int launch_tile_bwd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream);
 int launch_lse_merge(const float* o_parts, const float* lse_parts, int k_parts,
@@ -32,8 +30,6 @@ int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, l
 int make_map_f32_dq_flat(CUtensorMap* m, const float* ptr, int h, int rows, int bh,
                          long long s_row, long long s_bh, int box_rows, int box_cols = 0);
 int bwd_q_tile_rows(int h);
-int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
-                  const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream);
 int launch_poison(int mode, int num_sms, cudaStream_t stream);
 int launch_bench_umma(int variant, int iters, long long* out, int ctas, cudaStream_t stream);
 int launch_selftest_umma(const void* a, const void* b, float* d, int n, int b_mn_major,

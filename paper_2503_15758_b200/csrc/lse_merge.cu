@@ -125,8 +125,11 @@ __global__ void __launch_bounds__(256) bwd_finalize_kernel(const float* __restri
     const long long rr = e / h;
     const int r = (int)(rr % n);
     const int b = (int)(rr / n);
-    float4 v = *reinterpret_cast<const float4*>(acc + b * asbh + (long long)r * asrow + c);
-    v.x *= scale; v.y *= scale; v.z *= scale; v.w *= scale;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);  // acc == nullptr: zero fill
+    if (acc != nullptr) {
+      v = *reinterpret_cast<const float4*>(acc + b * asbh + (long long)r * asrow + c);
+      v.x *= scale; v.y *= scale; v.z *= scale; v.w *= scale;
+    }
     const long long dst = b * sbh + (long long)r * srow + c;
     if (out_dtype == A2D_F32) {
       *reinterpret_cast<float4*>(reinterpret_cast<float*>(dq) + dst) = v;

@@ -61,15 +61,9 @@ A2D_DEV uint32_t mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok;
 }
-A2D_DEV uint32_t mbar_try_wait_hint(uint32_t bar, uint32_t parity);
 A2D_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
-#ifdef A2D_X_SLEEPWAIT
-  while (!mbar_try_wait_hint(bar, parity)) {
-  }
-#else
   while (!mbar_try_wait(bar, parity)) {
   }
-#endif
 }
 // try_wait with a suspend-time hint: the waiting thread is parked by the
 // hardware until the phase completes (or the hint expires) instead of

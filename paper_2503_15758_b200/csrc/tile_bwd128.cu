@@ -1,9 +1,10 @@
-// tile_bwd128.cu — Attention2D tile backward for head dim 128 on sm_100a.
+// tile_bwd128.cu — Attention2D tile backward on sm_100a (any head dim <= 128;
+// the tiles are 128 wide and columns past h are TMA zero fill).
 //
-// Same recurrence as tile_bwd.cu (the reference's flash_backward,
-// numpy_backend.py:46-62) but shaped so that EVERY tcgen05.mma has N = 128,
-// the shape that runs at the full 8192 flop/clk/SM (tools/umma_rate.py: the
-// N = 64 shapes of the 64-query design are shared-memory bound at 61-70%).
+// The reference's flash_backward recurrence (numpy_backend.py:46-62), shaped
+// so that EVERY tcgen05.mma has N = 128, the shape that runs at the full
+// 8192 flop/clk/SM (tools/umma_rate.py: N = 64 shapes are shared-memory
+// bound at 61-70%).
 //
 // One CTA = one 128-key tile of one head; it sweeps 128-query tiles:
 //   S^T  = K Q_i^T            -> TMEM X      (SS, M128 N128)
@@ -31,13 +32,8 @@
 #include "kernels.h"
 
 // exponential pairs of the P phase evaluated on the FMA-pipe polynomial
-#if defined(B2X_POLY0)
-#define B_POLY(c) false
-#elif defined(B2X_POLY1OF8)
-#define B_POLY(c) ((((c) >> 1) & 7) == 7)
-#else
+// (one in four; 0 and 1/8 measured equal)
 #define B_POLY(c) ((((c) >> 1) & 3) == 3)
-#endif
 
 namespace a2d {
 namespace {
@@ -56,10 +52,7 @@ constexpr int OFF_DS = OFF_DO + TILE_B;
 // bulk-reduce throughput (~20 B/clk measured) is what bounds this kernel:
 // 4 x 16-row buffers measured 1-3% faster than 2 x 32, 8 x 8 16% slower, and
 // moving rows to red.global.add from registers is slower still.
-#ifndef B2_DQ_BUFS
-#define B2_DQ_BUFS 4
-#endif
-constexpr int DQ_BUFS = B2_DQ_BUFS;
+constexpr int DQ_BUFS = 4;
 constexpr int DQ_ROWS = 64 / DQ_BUFS;
 constexpr int DQ_ROUNDS = 128 / DQ_ROWS;
 constexpr int DQ_BUF_BYTES = DQ_ROWS * 128 * 4;
@@ -130,11 +123,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   TileRange qr;
   query_range(p.q_map, p.nq, causal, kt.gmin, qr, TILE);
   const int n_tiles = qr.total;
-#ifdef A2D_X_NOROT
-  const int qrot = causal ? 0 : kt_idx;
-#else
   const int qrot = kt_idx;  // rotated q sweep: co-resident CTAs reduce into different dQ rows
-#endif
 
   // ---------------------------------------------------------------- MMA issue
   // Warp-level helpers (one elected lane issues; whole warp converged):
@@ -453,10 +442,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (p.dkv_dtype == A2D_F32) {
         float* dst = reinterpret_cast<float*>(base) + off;
 #pragma unroll
-        for (int e = 0; e < 32; e += 4)
-          if (c * 32 + e < p.h)
-            *reinterpret_cast<float4*>(dst + e) =
-                make_float4(v[e] * mul, v[e + 1] * mul, v[e + 2] * mul, v[e + 3] * mul);
+        for (int e = 0; e < 32; e += 4) {
+          if (c * 32 + e >= p.h) continue;
+          float4 w = make_float4(v[e] * mul, v[e + 1] * mul, v[e + 2] * mul, v[e + 3] * mul);
+          if (p.accumulate_dkv) {
+            const float4 o = *reinterpret_cast<const float4*>(dst + e);
+            w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+          }
+          *reinterpret_cast<float4*>(dst + e) = w;
+        }
       } else {
         __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(base) + off;
 #pragma unroll
@@ -476,9 +470,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ------------------------------------------------------------ dQ drain
     const int quarter = warp & 3;
     const int h = quarter * 32 + lane;  // TMEM lane = head dim of dQ^T
-#ifdef B2X_DQ_BULK
-    const bool dq_flat = p.h == 128 && p.dq_stride_row == 128 && p.q_map.nblocks == 1;
-#endif
     const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
     int round = 0;
     TileCursor cur;
@@ -508,28 +499,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
-#ifdef A2D_X_NO_DQ
-        if (false) {
-#elif defined(A2D_X_HALF_DQ)
-        if (h == 0 && r < DQ_ROUNDS / 2) {
-#else
         if (h == 0) {
-#endif
-#ifdef B2X_DQ_EVICT_LAST
-          tma_reduce_add_3d_g_hint(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh, l2_policy_evict_last());
-#elif defined(B2X_DQ_BULK)
-          if (dq_flat) {  // contiguous rows: one plain bulk reduce per round
-            const int r0 = qrow + DQ_ROWS * r;
-            const int nr = min(DQ_ROWS, p.nq - r0);
-            if (nr > 0)
-              bulk_reduce_add_f32(p.dq_acc + (long long)bh * p.dq_stride_bh + (long long)r0 * 128,
-                                  buf, uint32_t(nr) * 512u);
-          } else {
-            tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);
-          }
-#else
           tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);
-#endif
           bulk_commit_group();
         }
       }
@@ -547,7 +518,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 }  // namespace
 
-int launch_bwd128(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
+int bwd_q_tile_rows(int) { return TILE; }
+
+int launch_tile_bwd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                   const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream) {
   static bool configured[64] = {false};
   int dev = 0;

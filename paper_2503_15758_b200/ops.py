@@ -245,12 +245,14 @@ def bwd_preprocess(o: torch.Tensor, dout: torch.Tensor) -> torch.Tensor:
 def tile_backward(q, k, v, dout, lse, delta, *, causal: bool, scale: float,
                   q_index: TokenIndex | None = None, k_index: TokenIndex | None = None,
                   dq_acc: torch.Tensor | None = None, dk: torch.Tensor | None = None,
-                  dv: torch.Tensor | None = None, dkv_dtype: torch.dtype = torch.float32):
+                  dv: torch.Tensor | None = None, dkv_dtype: torch.dtype = torch.float32,
+                  accumulate_dkv: bool = False):
     """Gradient contributions of the keys in k/v for the rows of q, given the
     GLOBAL (lse, delta) statistics of those rows (attention.py:225-257).
 
     dq_acc (fp32, unscaled dS K) is accumulated into; dk (scaled) and dv are
-    written, one per QUERY head (with GQA the caller sums each group).
+    written, one per QUERY head (with GQA the caller sums each group), or,
+    with accumulate_dkv, added to the fp32 dk / dv already there.
     Returns (dq_acc, dk, dv).
     """
     lib = _lib.load()
@@ -267,9 +269,13 @@ def tile_backward(q, k, v, dout, lse, delta, *, causal: bool, scale: float,
         raise ShapeError("lse / delta must be contiguous")
     qi = q_index if q_index is not None else TokenIndex.contiguous(nq)
     ki = k_index if k_index is not None else TokenIndex.contiguous(nk)
+    if qi.n != nq or ki.n != nk:
+        raise ShapeError("index maps do not match the row counts")
     qi, ki = _pair_maps(qi, ki, causal, q.device)
     if dq_acc is None:
         dq_acc = torch.zeros((bh, nq, h), dtype=torch.float32, device=q.device)
+    if accumulate_dkv and (dk is None or dv is None or dk.dtype != torch.float32):
+        raise ShapeError("accumulate_dkv needs existing fp32 dk / dv")
     if dk is None:
         dk = torch.empty((bh, nk, h), dtype=dkv_dtype, device=q.device)
     if dv is None:
@@ -292,6 +298,7 @@ def tile_backward(q, k, v, dout, lse, delta, *, causal: bool, scale: float,
     a.causal = int(bool(causal))
     a.scale = float(scale)
     a.dkv_dtype = _dtype_code(dk.dtype)
+    a.accumulate_dkv = int(bool(accumulate_dkv))
     a.q_map, a.k_map = qi.to_c(), ki.to_c()
     a.kv_group = group
     _lib.check(lib.a2d_tile_bwd(a, _stream(q)), "a2d_tile_bwd")

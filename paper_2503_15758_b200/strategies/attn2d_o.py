@@ -217,12 +217,13 @@ class Attention2DO:
         self.ops.bwd_finalize(_heads(dq_acc), self.scale, out=_heads(dq_p))
         return dq_p, dk_p.to(torch.bfloat16), dv_p.to(torch.bfloat16)
 
-    def _bwd_tile(self, bundle, q_index, k, v, k_index, dq, dk, dv):
+    def _bwd_tile(self, bundle, q_index, k, v, k_index, dq, dk, dv, accumulate=False):
         q_b, do_b, st_b = bundle
         self.ops.tile_backward(_heads(q_b), _heads(k), _heads(v), _heads(do_b),
                                st_b[..., 0].t().contiguous(), st_b[..., 1].t().contiguous(),
                                causal=self.causal, scale=self.scale, q_index=q_index,
-                               k_index=k_index, dq_acc=_heads(dq), dk=_heads(dk), dv=_heads(dv))
+                               k_index=k_index, dq_acc=_heads(dq), dk=_heads(dk), dv=_heads(dv),
+                               accumulate_dkv=accumulate)
 
     def _row_sweep_bwd(self, bundle_next, k_g, v_g, dk_g, dv_g):
         """gthr_cmpt_sctr_bwd (:314-372) with cmpt_sctr_bwd (:248-311) for the
@@ -233,8 +234,6 @@ class Attention2DO:
         bh, h = k_g.shape[1], k_g.shape[2]
         bundle, bw = bundle_next
         wait_all(bw)
-        tmp_k = torch.empty_like(dk_g)
-        tmp_v = torch.empty_like(dv_g)
         dq_recv = torch.empty((L, bh, h), dtype=torch.float32, device=dev)
         scat = None
         dk_fin = dv_fin = None
@@ -247,10 +246,9 @@ class Attention2DO:
                                     async_op=True)
             dq_i = torch.zeros((L, bh, h), dtype=torch.float32, device=dev)
             if i < g.pc - 1 or g.pr == 1:
-                self._bwd_tile(bundle, self._qblock(cc), k_g, v_g, self.k_index, dq_i, tmp_k,
-                               tmp_v)
-                dk_g.add_(tmp_k)
-                dv_g.add_(tmp_v)
+                # dK/dV of the gathered keys accumulate in place (kernel accumulate mode)
+                self._bwd_tile(bundle, self._qblock(cc), k_g, v_g, self.k_index, dq_i, dk_g,
+                               dv_g, accumulate=True)
                 if i == g.pc - 1:
                     dk_fin, dv_fin = dk_g, dv_g
             else:
@@ -278,17 +276,15 @@ class Attention2DO:
         the own slice r last (cmpt_sctr_bwd, :248-311)."""
         comm, g, L = self.comm, self.grid, self.L
         r = comm.r
-        dk_s = torch.empty((L,) + tuple(dk_g.shape[1:]), dtype=torch.float32, device=dk_g.device)
-        dv_s = torch.empty_like(dk_s)
-        inc_k = torch.empty_like(dk_s)
-        inc_v = torch.empty_like(dk_s)
+        inc_k = inc_v = None
         scat = None
         for j in list(range(1, g.pr)) + [0]:
             s = (r + j) % g.pr
+            # this bundle's contribution is added in place to slice s of the
+            # column sweep's dK/dV (kernel accumulate mode)
+            dk_s, dv_s = self._blk(dk_g, s), self._blk(dv_g, s)
             self._bwd_tile(bundle, q_index, self._blk(k_g, s), self._blk(v_g, s), self._kblock(s),
-                           dq_i, dk_s, dv_s)
-            dk_s.add_(self._blk(dk_g, s))
-            dv_s.add_(self._blk(dv_g, s))
+                           dq_i, dk_s, dv_s, accumulate=True)
             if scat is not None:
                 wait_all(scat)
                 comm.buf_close("dkv")
@@ -301,5 +297,4 @@ class Attention2DO:
             _, scat = comm.exchange([dk_s, dv_s], self.up, self.down, "scatter_dkv",
                                     async_op=True, recv_into=[nk, nv])
             inc_k, inc_v = nk, nv
-            dk_s, dv_s = torch.empty_like(dk_s), torch.empty_like(dv_s)
         raise AssertionError("unreachable")

@@ -65,8 +65,8 @@ class RingAttention:
         delta = self.ops.bwd_preprocess(_heads(saved.o), _heads(do_p))
         lse = saved.lse.t().contiguous()
         dq_acc = torch.zeros((rows, bh, h), dtype=torch.float32, device=do_p.device)
-        dk_acc = torch.zeros((rows, bh, h), dtype=torch.float32, device=do_p.device)
-        dv_acc = torch.zeros_like(dk_acc)
+        dk_acc = torch.empty((rows, bh, h), dtype=torch.float32, device=do_p.device)
+        dv_acc = torch.empty_like(dk_acc)
         dk_tmp = torch.empty_like(dk_acc)
         dv_tmp = torch.empty_like(dk_acc)
         cur_k, cur_v, src = saved.k, saved.v, self.rank
@@ -76,15 +76,23 @@ class RingAttention:
             if step < self.p - 1:
                 (nk, nv), kv_work = comm.exchange([cur_k, cur_v], self.nxt, self.prv, "ring_kv",
                                                   True)
+            # Step 0 writes the own block's accumulator directly.  Later steps
+            # write a scratch block and add it once the travelling accumulator
+            # of block `src` has arrived: accumulating in place would make the
+            # kernel wait for that hop (its sender finishes the previous step
+            # at the same time as this rank), exposing the transfer.
+            first = step == 0
             self.ops.tile_backward(_heads(saved.q), _heads(cur_k), _heads(cur_v), _heads(do_p),
                                    lse, delta, causal=self.causal, scale=self.scale,
                                    q_index=self.q_index, k_index=ring_index(self.n, self.p, src),
-                                   dq_acc=_heads(dq_acc), dk=_heads(dk_tmp), dv=_heads(dv_tmp))
+                                   dq_acc=_heads(dq_acc), dk=_heads(dk_acc if first else dk_tmp),
+                                   dv=_heads(dv_acc if first else dv_tmp))
             if acc_work is not None:  # the accumulator of block `src` arrives from prev
                 wait_all(acc_work[1])
                 dk_acc, dv_acc = acc_work[0]
-            dk_acc.add_(dk_tmp)
-            dv_acc.add_(dv_tmp)
+            if not first:
+                dk_acc.add_(dk_tmp)
+                dv_acc.add_(dv_tmp)
             if self.p > 1:
                 # forward this block's accumulator (after P-1 hops it is one short of home)
                 acc_work = comm.exchange([dk_acc, dv_acc], self.nxt, self.prv,

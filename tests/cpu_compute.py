@@ -65,15 +65,19 @@ def bwd_preprocess(o, dout):
 
 
 def tile_backward(q, k, v, dout, lse, delta, *, causal, scale, q_index=None, k_index=None,
-                  dq_acc=None, dk=None, dv=None, dkv_dtype=torch.float32):
+                  dq_acc=None, dk=None, dv=None, dkv_dtype=torch.float32, accumulate_dkv=False):
     s = _scores(q, k, causal, scale, q_index, k_index)
     l = lse.double()
     p = torch.exp(s - torch.where(torch.isinf(l), torch.full_like(l, float("inf")), l)[..., None])
     dp = torch.einsum("bqh,bkh->bqk", dout.double(), v.double())
     ds = p * (dp - delta.double()[..., None])
     dq_acc.add_(torch.einsum("bqk,bkh->bqh", ds, k.double()).to(dq_acc.dtype))
-    dk.copy_((torch.einsum("bqk,bqh->bkh", ds, q.double()) * scale).to(dk.dtype))
-    dv.copy_(torch.einsum("bqk,bqh->bkh", p, dout.double()).to(dv.dtype))
+    gk = torch.einsum("bqk,bqh->bkh", ds, q.double()) * scale
+    gv = torch.einsum("bqk,bqh->bkh", p, dout.double())
+    if accumulate_dkv:
+        gk, gv = gk + dk.double(), gv + dv.double()
+    dk.copy_(gk.to(dk.dtype))
+    dv.copy_(gv.to(dv.dtype))
     return dq_acc, dk, dv
 
 

@@ -55,11 +55,11 @@ def bwd_preprocess(o, dout):
 
 
 def tile_backward(q, k, v, dout, lse, delta, *, causal, scale, q_index=None, k_index=None,
-                  dq_acc=None, dk=None, dv=None, dkv_dtype=torch.float32):
+                  dq_acc=None, dk=None, dv=None, dkv_dtype=torch.float32, accumulate_dkv=False):
     dqg, dkg, dvg = ops.tile_backward(_g(q), _g(k), _g(v), _g(dout), _g(lse), _g(delta),
                                       causal=causal, scale=scale, q_index=q_index,
                                       k_index=k_index, dq_acc=_g(dq_acc), dk=_g(dk), dv=_g(dv),
-                                      dkv_dtype=dkv_dtype)
+                                      dkv_dtype=dkv_dtype, accumulate_dkv=accumulate_dkv)
     torch.cuda.synchronize()
     return _back(dq_acc, dqg), _back(dk, dkg), _back(dv, dvg)
 

@@ -3,7 +3,7 @@
 set -e
 TX=${1:-3}; TY=${2:-5}
 R=/root/repo/paper_2503_15758_b200/csrc
-rm -rf /tmp/xt && mkdir -p /tmp/xt && cp $R/*.cu $R/*.cuh $R/*.h /tmp/xt/
+rm -rf /tmp/xt && mkdir -p /tmp/xt && cp $R/*.cu $R/*.cuh $R/*.h $R/Makefile /tmp/xt/
 sed -i 's|../../include/attn2d_b200.h|/root/repo/include/attn2d_b200.h|' /tmp/xt/*
 python3 - <<'PY'
 p='/tmp/xt/tile_bwd128.cu'; s=open(p).read()
@@ -34,5 +34,5 @@ extern "C" int a2d_trace_dump(long long* host) { return (int)cudaMemcpyFromSymbo
 ''', 1)
 open(p,'w').write(s)
 PY
-cd /tmp/xt && /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -DTX=$TX -DTY=$TY $XFLAGS -shared -o /root/repo/xlib/lib_TRACE$XSUF.so abi.cu tile_fwd.cu tile_fwd2.cu tile_bwd.cu tile_bwd128.cu lse_merge.cu selftest.cu -lcudart_static -lrt -ldl -lpthread
+cd /tmp/xt && /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -DTX=$TX -DTY=$TY $XFLAGS -shared -o /root/repo/xlib/lib_TRACE$XSUF.so $(sed -n "s/^SRCS := //p" Makefile) -lcudart_static -lrt -ldl -lpthread
 echo built

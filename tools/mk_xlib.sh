@@ -7,6 +7,6 @@ R=/root/repo/paper_2503_15758_b200/csrc
 mkdir -p /root/repo/xlib
 cd $R && /usr/local/cuda/bin/nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a \
   -Xcompiler -fPIC --expt-relaxed-constexpr $FL -shared -o /root/repo/xlib/lib_$NAME.so \
-  abi.cu tile_fwd.cu tile_fwd2.cu tile_bwd.cu tile_bwd128.cu lse_merge.cu selftest.cu \
+  $(sed -n "s/^SRCS := //p" Makefile) \
   -lcudart_static -lrt -ldl -lpthread
 echo built xlib/lib_$NAME.so
