@@ -205,9 +205,98 @@ def gpu_parity_cases():
     np.savez_compressed(OUT / "gpu_parity.npz", **out)
 
 
+def dropin_cases():
+    """The reference's own attention-API test vectors on bf16-rounded inputs
+    (so a bf16 kernel sees exactly the values the reference computed on),
+    for the drop-in tests of the B200 path (tests/test_dropin.py):
+    test_attention.py:123-157 (forward, index subsets, masked rows),
+    :289-328 (backward, key-subset partial sums), test_kernels.py:124-137
+    (streaming continuation), SPEC.md:132-133 (known answer), and the
+    strategy entry points run_forward / run_backward at p in {1, 4}."""
+    out = {}
+    r = lambda seed, *shape: bf16_round(np.random.default_rng(seed).uniform(-1, 1, shape))  # noqa
+    # forward vs blocks and masks (test_attention.py:123-130)
+    q, k, v = r(40, 7, 4), r(41, 7, 4), r(42, 7, 4)
+    out.update(fw_q=q, fw_k=k, fw_v=v)
+    for mname, mask in (("none", MaskSpec.none()), ("causal", MaskSpec.causal())):
+        for block in (1, 3, 64):
+            part = flash_attn_forward(TokenShard(q, np.arange(7)), TokenShard(k, np.arange(7)),
+                                      TokenShard(v, np.arange(7)), mask, 1.0, block)
+            out[f"fw_{mname}_b{block}_o"] = finalize(part)
+            out[f"fw_{mname}_b{block}_lse"] = part.logsumexp
+    # index subsets (test_attention.py:136-145) and masked rows (:147-157)
+    qi, ki = np.array([3, 9, 17]), np.array([2, 9, 12, 20])
+    q, k, v = r(43, 3, 3), r(44, 4, 3), r(45, 4, 3)
+    part = flash_attn_forward(TokenShard(q, qi), TokenShard(k, ki), TokenShard(v, ki),
+                              MaskSpec.causal())
+    out.update(sub_q=q, sub_k=k, sub_v=v, sub_qi=qi, sub_ki=ki, sub_o=finalize(part),
+               sub_lse=part.logsumexp)
+    q, k, v = r(46, 2, 2), r(47, 2, 2), r(48, 2, 2)
+    part = flash_attn_forward(TokenShard(q, [0, 8]), TokenShard(k, [4, 5]),
+                              TokenShard(v, [4, 5]), MaskSpec.causal())
+    out.update(msk_q=q, msk_k=k, msk_v=v, msk_lse=part.logsumexp,
+               msk_o1=part.n[1] / part.d[1])
+    # streaming continuation (test_kernels.py:124-137), kernel level
+    q, k, v, qi, ki = (bf16_round(x) if x.dtype == np.float64 else x
+                       for x in random_problem(15))
+    m = np.full(q.shape[0], -np.inf)
+    nacc, d = np.zeros_like(q), np.zeros(q.shape[0])
+    kernels.flash_forward(q, k, v, qi, ki, False, 1.0, 64, m, nacc, d)
+    out.update(cont_q=q, cont_k=k, cont_v=v, cont_qi=qi, cont_ki=ki, cont_o=nacc / d[:, None],
+               cont_lse=m + np.log(d))
+    # backward full range (test_attention.py:289-300) and key-subset partial
+    # sums (:302-328), both masks
+    for mname, mask in (("none", MaskSpec.none()), ("causal", MaskSpec.causal())):
+        n, h = 6, 3
+        q, k, v, do = r(78, n, h), r(79, n, h), r(80, n, h), r(81, n, h)
+        idx = np.arange(n)
+        part = flash_attn_forward(TokenShard(q, idx), TokenShard(k, idx), TokenShard(v, idx),
+                                  mask)
+        o = finalize(part)
+        dq, dk, dv = flash_attn_backward(TokenShard(q, idx), TokenShard(k, idx),
+                                         TokenShard(v, idx), o, do, part.m, part.d, mask)
+        out.update({f"bw_{mname}_{x}": y for x, y in
+                    (("q", q), ("k", k), ("v", v), ("do", do), ("o", o), ("lse", part.logsumexp),
+                     ("dq", dq), ("dk", dk), ("dv", dv))})
+    # mid-size tile parity (h = 64 / 128, scale 1/sqrt(h)), kernel level
+    for tag, n, h, causal, seed in (("mid_h64_causal", 256, 64, True, 201),
+                                    ("mid_h128_none", 256, 128, False, 202)):
+        q, k, v, do = (bf16_round(x) for x in gen(n, h, seed))
+        idx = np.arange(n)
+        mask = MaskSpec.causal() if causal else MaskSpec.none()
+        sc = 1.0 / np.sqrt(h)
+        part = flash_attn_forward(TokenShard(q, idx), TokenShard(k, idx), TokenShard(v, idx),
+                                  mask, sc)
+        o = finalize(part)
+        dq, dk, dv = flash_attn_backward(TokenShard(q, idx), TokenShard(k, idx),
+                                         TokenShard(v, idx), o, do, part.m, part.d, mask, sc)
+        out.update({f"{tag}_{x}": y for x, y in
+                    (("q", q), ("k", k), ("v", v), ("do", do), ("o", o), ("lse", part.logsumexp),
+                     ("dq", dq), ("dk", dk), ("dv", dv))})
+        out[f"{tag}_meta"] = np.array([n, h, int(causal), sc])
+    # strategy entry points (strategies/__init__.py:40-46) on the simulated grid
+    for name in ("attn2d_no", "attn2d_o", "ring"):
+        for p in (1, 4):
+            for causal in (False, True):
+                n, h = 64, 8
+                mask = MaskKind.CAUSAL if causal else MaskKind.NONE
+                cfg = DistAttnConfig(n=n, h=h, p=p, mask=mask, scale=h ** -0.5)
+                q, k, v, do = (bf16_round(x) for x in gen(n, h, seed=700 + p))
+                fwd = run_forward(name, cfg, q, k, v)
+                bwd = run_backward(name, cfg, fwd.saved, do)
+                tag = f"st_{name}_p{p}_{'causal' if causal else 'none'}"
+                out.update({f"{tag}_o": fwd.o, f"{tag}_dq": bwd.dq, f"{tag}_dk": bwd.dk,
+                            f"{tag}_dv": bwd.dv})
+                out[f"st_in_p{p}"] = np.stack([q, k, v, do])
+    # fp32 storage: inputs are bf16 values (exact), outputs far more precise
+    # than the bf16-kernel tolerance they are checked at
+    out = {k: (v.astype(np.float32) if v.dtype == np.float64 else v) for k, v in out.items()}
+    np.savez_compressed(OUT / "dropin.npz", **out)
+
+
 if __name__ == "__main__":
     only = sys.argv[1:]
-    for fn in (tile_cases, merge_cases, strategy_cases, gpu_parity_cases):
+    for fn in (tile_cases, merge_cases, strategy_cases, gpu_parity_cases, dropin_cases):
         if not only or fn.__name__ in only:
             fn()
     for f in sorted(OUT.glob("*.npz")):

@@ -23,16 +23,24 @@ ev = [("const int qrow0 = cur.row0(p.q_map);", 0, 4, 'after'),
       ("mbar_wait(bar(B_DQFULL), i & 1);", 13, 12, 'after'),
       ("mbar_arrive(bar(B_DQFREE));", 14, 12, 'before'),
       ("bulk_commit_group();", 15, 12, 'after')]
+# the same P/dS events for a warp of the second warpgroup (warp 8)
+ev2 = [("mbar_arrive(bar(B_PREADY));", 16, 8, 'before'),
+       ("mbar_arrive(bar(B_DSREADY));", 17, 8, 'before'),
+       ("mbar_wait(bar(B_SFULL), i & 1);", 18, 8, 'after'),
+       ("mbar_wait(bar(B_DPFULL), i & 1);", 19, 8, 'after')]
 for pat, e, w, where in ev:
     assert pat in s, pat
     t = f"TRACE({e}, i, {w});"
     s = s.replace(pat, (pat + " " + t) if where == 'after' else (t + " " + pat), 1)
+for pat, e, w, where in ev2:
+    t = f"TRACE({e}, i, {w});"
+    s = s.replace(pat, (pat + " " + t) if where == 'after' else (t + " " + pat), 1)
 s = s.replace('#include "kernels.h"\n', '''#include "kernels.h"
-__device__ long long g_trace[16][1024];
+__device__ long long g_trace[24][1024];
 #define TRACE(ev, i, w) do { if (blockIdx.x == TX && blockIdx.y == TY && warp == (w) && (threadIdx.x & 31) == 0 && (i) < 1024) g_trace[ev][i] = clock64(); } while (0)
 extern "C" int a2d_trace_dump(long long* host) { return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace)); }
 ''', 1)
 open(p,'w').write(s)
 PY
-cd /tmp/xt && /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -DTX=$TX -DTY=$TY $XFLAGS -shared -o /root/repo/xlib/lib_TRACE$XSUF.so $(sed -n "s/^SRCS := //p" Makefile) -lcudart_static -lrt -ldl -lpthread
+mkdir -p /root/repo/xlib2 && cd /tmp/xt && /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -DTX=$TX -DTY=$TY $XFLAGS -shared -o /root/repo/xlib2/lib_TRACE$XSUF.so $(sed -n "s/^SRCS := //p" Makefile) -lcudart_static -lrt -ldl -lpthread
 echo built

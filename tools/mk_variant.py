@@ -1,0 +1,65 @@
+"""Build A/B variants of the library from patched copies of csrc/ (the product
+sources stay free of experiment switches).
+
+    python tools/mk_variant.py NAME [NAME ...]      -> xlib2/lib_NAME.so
+    A2D_LIB_PATH=xlib2/lib_NAME.so python tools/perf_tile.py bwd 32768 32 128 1
+
+Each variant is a list of (file, old, new) string replacements; an `old`
+that is not found aborts the build.  xlib2/ is scratch (git-ignored).
+"""
+
+from __future__ import annotations
+
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+CSRC = ROOT / "paper_2503_15758_b200" / "csrc"
+OUT = ROOT / "xlib2"
+
+B = "tile_bwd128.cu"
+F = "tile_fwd2.cu"
+VARIANTS: dict[str, list[tuple[str, str, str]]] = {
+    "base": [],
+    # upper bound: no dQ reduce at all (wrong results)
+    "nodq": [(B, "          tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);",
+              "          if (false) tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);")],
+    # half the dQ bytes (wrong results)
+    "halfdq": [(B, "          tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);",
+                "          if (r < DQ_ROUNDS / 2) tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);")],
+    # half the staging bytes in flight (2 x 8 KB instead of 4 x 8 KB)
+    "stage16k": [(B, "constexpr int DQ_BUFS = 4;\nconstexpr int DQ_ROWS = 64 / DQ_BUFS;",
+                  "constexpr int DQ_BUFS = 2;\nconstexpr int DQ_ROWS = 16;")],
+    # P phase: half of the exponential pairs on the FMA-pipe polynomial
+    "poly2": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)", "#define B_POLY(c) (((c) >> 1) & 1)")],
+    "poly38": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)",
+                "#define B_POLY(c) ((((c) >> 1) & 7) == 1 || (((c) >> 1) & 7) == 4 || (((c) >> 1) & 7) == 6)")],
+}
+
+
+def build(name: str) -> Path:
+    patches = VARIANTS[name]
+    work = Path("/tmp") / f"a2d_var_{name}"
+    if work.exists():
+        shutil.rmtree(work)
+    shutil.copytree(CSRC, work / "pkg" / "csrc", ignore=shutil.ignore_patterns("build"))
+    shutil.copytree(ROOT / "include", work / "include")
+    for fname, old, new in patches:
+        p = work / "pkg" / "csrc" / fname
+        s = p.read_text()
+        if old not in s:
+            raise SystemExit(f"{name}: patch target not found in {fname}: {old[:60]!r}")
+        p.write_text(s.replace(old, new))
+    OUT.mkdir(exist_ok=True)
+    lib = OUT / f"lib_{name}.so"
+    mk = work / "pkg" / "csrc" / "Makefile"
+    mk.write_text(mk.read_text().replace("LIB := ../libattn2d_b200.so", f"LIB := {lib}"))
+    subprocess.run(["make", "-C", str(work / "pkg" / "csrc"), "-j8", "-s"], check=True)
+    return lib
+
+
+if __name__ == "__main__":
+    for n in sys.argv[1:] or list(VARIANTS):
+        print("built", build(n))
