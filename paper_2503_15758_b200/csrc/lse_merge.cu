@@ -63,11 +63,16 @@ __global__ void __launch_bounds__(256) lse_merge_kernel(
       for (int c = 0; c < (K > 0 ? K : kMaxParts); ++c) {
         // an empty partial (lse = -inf) contributes exactly nothing, whatever its O holds
         const float w = (mx == -INFINITY || l[c][r] == -INFINITY) ? 0.f : __expf(l[c][r] - mx);
+        // products rounded before they are summed (no FMA contraction), so a
+        // two-way merge is bitwise commutative like the reference's attn_fix
+        // (test_attention.py:203-210)
         tot += w;
-        acc.x = w != 0.f ? fmaf(w, v[c][r].x, acc.x) : acc.x;
-        acc.y = w != 0.f ? fmaf(w, v[c][r].y, acc.y) : acc.y;
-        acc.z = w != 0.f ? fmaf(w, v[c][r].z, acc.z) : acc.z;
-        acc.w = w != 0.f ? fmaf(w, v[c][r].w, acc.w) : acc.w;
+        if (w != 0.f) {
+          acc.x = __fadd_rn(acc.x, __fmul_rn(w, v[c][r].x));
+          acc.y = __fadd_rn(acc.y, __fmul_rn(w, v[c][r].y));
+          acc.z = __fadd_rn(acc.z, __fmul_rn(w, v[c][r].z));
+          acc.w = __fadd_rn(acc.w, __fmul_rn(w, v[c][r].w));
+        }
       }
       const float inv = tot > 0.f ? 1.f / tot : 0.f;
       acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;

@@ -34,6 +34,16 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
                   "constexpr int DQ_BUFS = 2;\nconstexpr int DQ_ROWS = 16;")],
     # P phase: half of the exponential pairs on the FMA-pipe polynomial
     "poly2": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)", "#define B_POLY(c) (((c) >> 1) & 1)")],
+    # TMA tensor STORE instead of reduce-add (wrong results): the L2 RMW cost
+    "dqstore": [(B, "          tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);",
+                 "          asm volatile(\"cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group"
+                 " [%0, {%2, %3, %4}], [%1];\" :: \"l\"(reinterpret_cast<uint64_t>(&tm_dq)),"
+                 " \"r\"(buf), \"r\"(0), \"r\"(qrow + DQ_ROWS * r), \"r\"(bh) : \"memory\");")],
+    # no wait for the staging buffer's previous reduce (races, wrong results)
+    "dqnowait": [(B, "        if (h == 0) bulk_wait_group_read<DQ_BUFS - 1>();", "")],
+    # forward: a quarter of the exponential pairs on the FMA polynomial
+    "fpoly4": [(F, "#define F2_POLY(jj) ((((jj) >> 1) & 7) == 7)", "#define F2_POLY(jj) ((((jj) >> 1) & 3) == 3)")],
+    "fpoly0": [(F, "#define F2_POLY(jj) ((((jj) >> 1) & 7) == 7)", "#define F2_POLY(jj) false")],
     "poly38": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)",
                 "#define B_POLY(c) ((((c) >> 1) & 7) == 1 || (((c) >> 1) & 7) == 4 || (((c) >> 1) & 7) == 6)")],
 }
