@@ -367,7 +367,7 @@ def run_dist(args, rank, world, dev, compute, mark, elapsed, sync, dtype=None):
         led = comm.ledger
         return {"ms": ms, "plan": plan, "kernels": timed.summary(elapsed, args.steps),
                 "bytes_out_per_step": led.bytes_out() / args.steps,
-                "msgs_per_step": sum(v[2] for v in led.rows.values()) / args.steps,
+                "msgs_per_step": led.msgs_out() / args.steps,
                 "ledger": led.as_dict()}
 
     main_grid = Grid2D(pr, pc) if args.strategy in ("attn2d_no", "attn2d_o") else Grid2D(1, world)

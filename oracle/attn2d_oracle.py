@@ -237,3 +237,34 @@ def attention_flops(n_q_k_pairs, h, heads=1, backward=True):
     """FLOP accounting of BASELINE.md §3: 4·H·U fwd, ×3.5 fwd+bwd."""
     f = 4.0 * h * n_q_k_pairs * heads
     return f * 3.5 if backward else f
+
+
+# ---------------------------------------------------------------------------
+# Exact schedule identities of the reference (costmodel.py:106-153)
+# ---------------------------------------------------------------------------
+
+def predicted_phase_words(strategy, n, h, p, phase_fwd, on_diagonal):
+    """Words one processor sends in one phase (costmodel.py:106-136): square
+    p = s^2 for the 2D schedules, (m, n, d) partials of h + 2 words, backward
+    bundles (q, o, d_out, m, d) of 3h + 2 words."""
+    rows = n // p
+    if strategy == "ring":
+        if phase_fwd:
+            return 2 * rows * h * (p - 1)
+        return 4 * rows * h * (p - 1) + (2 * rows * h if p > 1 else 0)
+    side = int(round(p ** 0.5))
+    assert side * side == p
+    transpose = 0 if on_diagonal else 2 * rows * h
+    if phase_fwd:
+        return (transpose + (side - 1) * rows * h + 2 * (side - 1) * rows * h
+                + (side - 1) * rows * (h + 2))
+    return (transpose + (side - 1) * rows * (3 * h + 2) + 2 * (side - 1) * rows * h
+            + (side - 1) * rows * h + 2 * (side - 1) * rows * h)
+
+
+def predicted_phase_msgs(strategy, n, h, p, phase_fwd, on_diagonal):
+    """Messages one processor sends in one phase (costmodel.py:139-153)."""
+    if strategy == "ring":
+        return (p - 1) if phase_fwd else (p - 1) + (1 if p > 1 else 0)
+    side = int(round(p ** 0.5))
+    return (0 if on_diagonal else 1) + (3 if phase_fwd else 4) * (side - 1)

@@ -27,19 +27,34 @@ from ..layouts import Grid2D
 
 @dataclass
 class ByteLedger:
-    rows: dict = field(default_factory=lambda: defaultdict(lambda: [0, 0, 0]))
+    """Per-rank traffic by (phase, op): bytes out / in, API calls, words
+    (elements) out and point-to-point messages out.  A collective over n
+    ranks counts n - 1 messages (the relay hops of the reference's
+    mesh.py:106-191 ledger); a send to one peer counts 1."""
 
-    def charge(self, phase: str, op: str, bytes_out: int, bytes_in: int):
+    rows: dict = field(default_factory=lambda: defaultdict(lambda: [0, 0, 0, 0, 0]))
+
+    def charge(self, phase: str, op: str, bytes_out: int, bytes_in: int, words_out: int = 0,
+               msgs_out: int = 1):
         row = self.rows[(phase, op)]
         row[0] += int(bytes_out)
         row[1] += int(bytes_in)
         row[2] += 1
+        row[3] += int(words_out)
+        row[4] += int(msgs_out)
 
     def bytes_out(self, phase: str | None = None) -> int:
         return sum(v[0] for (ph, _), v in self.rows.items() if phase in (None, ph))
 
+    def words_out(self, phase: str | None = None) -> int:
+        return sum(v[3] for (ph, _), v in self.rows.items() if phase in (None, ph))
+
+    def msgs_out(self, phase: str | None = None) -> int:
+        return sum(v[4] for (ph, _), v in self.rows.items() if phase in (None, ph))
+
     def as_dict(self) -> dict:
-        return {f"{ph}/{op}": {"bytes_out": v[0], "bytes_in": v[1], "calls": v[2]}
+        return {f"{ph}/{op}": {"bytes_out": v[0], "bytes_in": v[1], "calls": v[2],
+                               "words_out": v[3], "msgs_out": v[4]}
                 for (ph, op), v in sorted(self.rows.items())}
 
 
@@ -90,7 +105,8 @@ class GridComm:
             return (t, None) if async_op else t
         out = torch.empty((n * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
         work = dist.all_gather_into_tensor(out, t.contiguous(), group=group, async_op=async_op)
-        self.ledger.charge(self.phase, op, _nbytes(t) * (n - 1), _nbytes(t) * (n - 1))
+        self.ledger.charge(self.phase, op, _nbytes(t) * (n - 1), _nbytes(t) * (n - 1),
+                           t.numel() * (n - 1), n - 1)
         return (out, work) if async_op else out
 
     def row_all_gather(self, t, op="gather_q", async_op=False):
@@ -104,7 +120,8 @@ class GridComm:
             return (t, None) if async_op else t
         out = torch.empty((t.shape[0] // n,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
         t = t.contiguous()
-        self.ledger.charge(self.phase, op, _nbytes(out) * (n - 1), _nbytes(out) * (n - 1))
+        self.ledger.charge(self.phase, op, _nbytes(out) * (n - 1), _nbytes(out) * (n - 1),
+                           out.numel() * (n - 1), n - 1)
         if dist.get_backend(group) == "gloo":
             # gloo has no reduce_scatter: all_reduce and keep this rank's chunk
             work = dist.all_reduce(t, group=group)
@@ -126,7 +143,8 @@ class GridComm:
             return (t, None) if async_op else t
         t = t.contiguous()
         out = torch.empty_like(t)
-        self.ledger.charge(self.phase, op, _nbytes(t) // n * (n - 1), _nbytes(t) // n * (n - 1))
+        self.ledger.charge(self.phase, op, _nbytes(t) // n * (n - 1), _nbytes(t) // n * (n - 1),
+                           t.numel() // n * (n - 1), n - 1)
         work = dist.all_to_all_single(out, t, group=self.row_group, async_op=async_op)
         return (out, work) if async_op else out
 
@@ -146,7 +164,7 @@ class GridComm:
         ops += [dist.P2POp(dist.irecv, b, src) for b in recvs]
         reqs = dist.batch_isend_irecv(ops)
         nb = sum(_nbytes(t) for t in sends)
-        self.ledger.charge(self.phase, op, nb, nb)
+        self.ledger.charge(self.phase, op, nb, nb, sum(t.numel() for t in sends), 1)
         if async_op:
             return recvs, reqs
         for q in reqs:

@@ -41,7 +41,8 @@ def to_cyclic(x: torch.Tensor, comm: GridComm) -> torch.Tensor:
     send = torch.stack([parts[:, res] for res in order], dim=0).contiguous()
     recv = torch.empty_like(send)
     comm.ledger.charge(comm.phase, "to_cyclic", send.numel() // p * (p - 1) * send.element_size(),
-                       send.numel() // p * (p - 1) * send.element_size())
+                       send.numel() // p * (p - 1) * send.element_size(),
+                       send.numel() // p * (p - 1), p - 1)
     dist.all_to_all_single(recv.view(p * k, -1), send.view(p * k, -1), group=comm.world)
     return recv.reshape(p * k, *x.shape[1:])          # sources in order = global order
 
@@ -55,7 +56,8 @@ def from_cyclic(y: torch.Tensor, comm: GridComm) -> torch.Tensor:
     send = y.reshape(p, k, *y.shape[1:]).contiguous()  # block s: my rows inside chunk s
     recv = torch.empty_like(send)
     comm.ledger.charge(comm.phase, "from_cyclic", send.numel() // p * (p - 1) * send.element_size(),
-                       send.numel() // p * (p - 1) * send.element_size())
+                       send.numel() // p * (p - 1) * send.element_size(),
+                       send.numel() // p * (p - 1), p - 1)
     dist.all_to_all_single(recv.view(p * k, -1), send.view(p * k, -1), group=comm.world)
     # recv block d = chunk rows with residue order[d]; interleave back by residue
     order = [g.residue(*g.coord(d)) for d in range(p)]

@@ -44,6 +44,30 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
     # forward: a quarter of the exponential pairs on the FMA polynomial
     "fpoly4": [(F, "#define F2_POLY(jj) ((((jj) >> 1) & 7) == 7)", "#define F2_POLY(jj) ((((jj) >> 1) & 3) == 3)")],
     "fpoly0": [(F, "#define F2_POLY(jj) ((((jj) >> 1) & 7) == 7)", "#define F2_POLY(jj) false")],
+    # dQ = dS K (TMEM lane = query row) drained by 16-byte red.global.add.v4.f32
+    # straight from registers: no shared-memory staging, no TMA reduce
+    "dqred4": [
+        (B, "umma_bf16(tmem + TM_Y, kb + mofs(kk), dsb + mofs(kk), id_mnmn, kk > 0);",
+            "umma_bf16(tmem + TM_Y, dsb + mofs(kk), kb + mofs(kk), id_mnmn, kk > 0);"),
+        (B, """#pragma unroll
+      for (int r = 0; r < DQ_ROUNDS; ++r, ++round) {
+        const uint32_t buf = sb + OFF_DQ + (round % DQ_BUFS) * DQ_BUF_BYTES;""",
+            """const TileRef qtl = tile_ref(p.q_map, p.nq, qrow);
+      if (h < qtl.nvalid) {
+        float* dst = p.dq_acc + (long long)bh * p.dq_stride_bh + (long long)(qrow + h) * p.dq_stride_row;
+#pragma unroll
+        for (int c = 0; c < 128; c += 4)
+          if (c < p.h)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(dst + c),
+                         "f"(v[c]), "f"(v[c + 1]), "f"(v[c + 2]), "f"(v[c + 3]) : "memory");
+      }
+#pragma unroll
+      for (int r = 0; r < 0; ++r, ++round) {
+        const uint32_t buf = sb + OFF_DQ + (round % DQ_BUFS) * DQ_BUF_BYTES;"""),
+    ],
+    # no dQ drain work at all besides reading TMEM (wrong results): SMEM bound test
+    "nodqsts": [(B, "for (int r = 0; r < DQ_ROUNDS; ++r, ++round) {", "for (int r = 0; r < 0; ++r, ++round) {")],
+    "dqredT": [(B, "constexpr bool kDqRed = false;", "constexpr bool kDqRed = true;")],
     "poly38": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)",
                 "#define B_POLY(c) ((((c) >> 1) & 7) == 1 || (((c) >> 1) & 7) == 4 || (((c) >> 1) & 7) == 6)")],
 }
