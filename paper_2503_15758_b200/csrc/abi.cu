@@ -78,6 +78,11 @@ int make_map(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long long
 
 }  // namespace
 
+int make_map_bf16(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long long s_row,
+                  long long s_bh, const char* name, int box_rows) {
+  return make_map(m, ptr, h, rows, bh, s_row, s_bh, name, box_rows);
+}
+
 // fp32 [bh, rows, h] contiguous accumulator, box 32 x box_rows x 1, 128B swizzle
 // (the backward's dQ reduce-add target).
 int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, long long s_row,

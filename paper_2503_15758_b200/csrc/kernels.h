@@ -25,6 +25,8 @@ int launch_bwd_preprocess(const void* o, const void* dout, float* delta, long lo
 int launch_bwd_finalize(const float* dq_acc, long long asbh, long long asrow, void* dq,
                         int out_dtype, long long sbh, long long srow, int bh, int n, int h,
                         float scale, cudaStream_t stream);
+int make_map_bf16(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long long s_row,
+                  long long s_bh, const char* name, int box_rows);
 int make_map_f32_dq(CUtensorMap* m, const float* ptr, int h, int rows, int bh, long long s_row,
                     long long s_bh, int box_rows);
 int make_map_f32_dq_flat(CUtensorMap* m, const float* ptr, int h, int rows, int bh,
