@@ -58,33 +58,24 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
-// PAIR: a cluster of two CTAs shares every MMA (cta_group::2, M = 256): each
-// CTA keeps its own two query tiles but stages only HALF of every key /
-// value tile — keys 64r..64r+63 (the N half of Q K^T's B operand) and head
-// dims 64r..64r+63 (the N half of P V's B operand) — so shared-memory
-// traffic per key tile drops from 256 KB to 160 KB per SM.
-template <int HD, bool PAIR>
+template <int HD>
 struct F2Layout {
   static constexpr int SLAB = TILE * 128;  // one 128-row x 64-col bf16 slab
   static constexpr int SLABS = HD / 64;
   static constexpr int TILE_BYTES = SLAB * SLABS;
-  static constexpr int KROWS = PAIR ? TILE / 2 : TILE;  // key rows staged per CTA
-  static constexpr int KSLAB = KROWS * 128;
-  static constexpr int K_BYTES = KSLAB * SLABS;
-  static constexpr int V_BYTES = PAIR ? SLAB : TILE_BYTES;  // PAIR: this CTA's 64 head dims
-  static constexpr int KST = PAIR ? 4 : 3;  // 1-CTA: 2 stages measured equal; the third is slack
-  static constexpr int VST = PAIR ? 4 : (HD == 128 ? 2 : 3);
+  static constexpr int KST = 3;  // 2 stages measured equal; the third is slack
+  static constexpr int VST = HD == 128 ? 2 : 3;
   static constexpr int OFF_Q = 0;  // Q0, Q1
   static constexpr int OFF_K = OFF_Q + 2 * TILE_BYTES;
-  static constexpr int OFF_V = OFF_K + KST * K_BYTES;
-  static constexpr int OFF_BAR = OFF_V + VST * V_BYTES;
+  static constexpr int OFF_V = OFF_K + KST * TILE_BYTES;
+  static constexpr int OFF_BAR = OFF_V + VST * TILE_BYTES;
   static constexpr int B_Q = 0;
   static constexpr int B_KFULL = 1;
   static constexpr int B_KEMPTY = B_KFULL + KST;
   static constexpr int B_VFULL = B_KEMPTY + KST;
   static constexpr int B_VEMPTY = B_VFULL + VST;
   static constexpr int B_SFULL = B_VEMPTY + VST;  // [2]: S_t(j) computed (and PV_t(j-1) done)
-  static constexpr int B_PFULL = B_SFULL + 2;     // [2]: P_t(j) stored (128 (+4 peer) arrivals)
+  static constexpr int B_PFULL = B_SFULL + 2;     // [2]: P_t(j) stored (128 arrivals)
   static constexpr int B_ODONE = B_PFULL + 2;     // [2]: last PV_t done
   static constexpr int NBAR = B_ODONE + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
@@ -171,14 +162,13 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
 }
 
 constexpr int F2_THREADS = 384;  // producer/MMA warpgroup + 8 softmax warps
-constexpr bool kFwdPair = true;
 
-template <int HD, bool PAIR>
+template <int HD>
 __global__ void __launch_bounds__(F2_THREADS, 1)
     fwd2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ a2d_tile_fwd_args p,
                 int q_tiles) {
-  using L = F2Layout<HD, PAIR>;
+  using L = F2Layout<HD>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sb = smem_u32(smem);
   if ((sb & 1023) != 0) __trap();
@@ -188,19 +178,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   // the heaviest causal pairs of a head start first.
   const int bh = blockIdx.y;
   const int bh_kv = p.kv_group > 1 ? bh / p.kv_group : bh;  // GQA / MQA: shared k/v head
-  // PAIR: cluster cl (heaviest first) owns tile pairs 2c, 2c+1 (c = reversed
-  // cluster index); CTA rank r takes pair 2c + r, and both sweep the union
-  // of the two pairs' key ranges in the same rotated order
-  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
-  const int rev = PAIR ? int(gridDim.x / 2 - 1 - blockIdx.x / 2) : int(gridDim.x - 1 - blockIdx.x);
-  const int pair = PAIR ? 2 * rev + int(rank) : rev;
+  const int pair = gridDim.x - 1 - blockIdx.x;
   auto bar = [&](int i) { return sb + L::OFF_BAR + 8 * i; };
-  // waits on barriers that receive the peer CTA's arrivals / bytes use
-  // cluster-scope acquire
-  auto wait_bar = [&](int i, uint32_t parity) {
-    if constexpr (PAIR) mbar_wait_cluster(bar(i), parity);
-    else mbar_wait_sleep(bar(i), parity);
-  };
   const uint32_t TM_O0 = 256, TM_O1 = 256 + HD;
 
   if (threadIdx.x == 0) {
@@ -215,7 +194,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(bar(L::B_SFULL + t), 1);
-      mbar_init(bar(L::B_PFULL + t), PAIR ? 128 + 4 : 128);
+      mbar_init(bar(L::B_PFULL + t), 128);
       mbar_init(bar(L::B_ODONE + t), 1);
     }
     fence_mbar_init();
@@ -226,97 +205,65 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     tma_prefetch_desc(&tm_v);
   }
   if (warp == 1) {
-    if constexpr (PAIR) {
-      tmem_alloc_pair(sb + L::OFF_TMEMPTR, TMEM_COLS);
-      tmem_relinquish_pair();
-    } else {
-      tmem_alloc(sb + L::OFF_TMEMPTR, TMEM_COLS);
-      tmem_relinquish();
-    }
+    tmem_alloc(sb + L::OFF_TMEMPTR, TMEM_COLS);
+    tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR) cluster_sync();  // peer barriers initialised before any remote use
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + L::OFF_TMEMPTR);
 
   const bool causal = p.causal != 0;
   const int t0 = 2 * pair, t1 = 2 * pair + 1;
-  const bool has0 = t0 < q_tiles;  // false only for the peer of an odd last pair
   const bool has1 = t1 < q_tiles;
-  TileRef qt0;
-  qt0.row0 = p.nq;
-  qt0.nvalid = 0;
-  qt0.gmin = qt0.gmax = -(1ll << 62);
-  if (has0) qt0 = tile_ref(p.q_map, p.nq, t0 * TILE);
+  const TileRef qt0 = tile_ref(p.q_map, p.nq, t0 * TILE);
   TileRef qt1 = qt0;
   if (has1) qt1 = tile_ref(p.q_map, p.nq, t1 * TILE);
-  long long qmax = has1 ? max(qt0.gmax, qt1.gmax) : qt0.gmax;
-  if constexpr (PAIR) {  // the peer's tiles: both CTAs sweep one key range
-    const int pp = 2 * rev + int(rank ^ 1u);
-    for (int t = 2 * pp; t < 2 * pp + 2; ++t)
-      if (t < q_tiles) qmax = max(qmax, tile_ref(p.q_map, p.nq, t * TILE).gmax);
-  }
   TileRange kr;
-  key_range(p.k_map, p.nk, causal, qmax, kr);
+  key_range(p.k_map, p.nk, causal, has1 ? max(qt0.gmax, qt1.gmax) : qt0.gmax, kr);
   const int n_tiles = kr.total;
-  const int rot = rev;  // rotated key sweep
+  const int rot = pair;  // rotated key sweep
 
   if (warp < 4) {
     regs_dec<96>();
     if (warp == 0 && lane == 0 && n_tiles > 0) {
       // -------------------------------------------------------- producer
-      // PAIR: both CTAs load their halves; the bytes land on the leader's
-      // barriers, whose expected byte counts cover the pair
-      auto load = [&](uint32_t dst, const CUtensorMap* map, int b, int c0, int c1, int c2) {
-        if constexpr (PAIR) tma_load_3d_pair(dst, map, bar(b), c0, c1, c2);
-        else tma_load_3d(dst, map, bar(b), c0, c1, c2);
-      };
-      constexpr int NCTA = PAIR ? 2 : 1;
-      if (rank == 0) mbar_expect_tx(bar(L::B_Q), NCTA * 2 * L::TILE_BYTES);
-      // an absent tile loads out of bounds (zero fill), never read
-      const int r0 = has0 ? qt0.row0 : p.nq;
+      mbar_expect_tx(bar(L::B_Q), 2 * L::TILE_BYTES);
       for (int s = 0; s < L::SLABS; ++s) {
-        load(sb + L::OFF_Q + s * L::SLAB, &tm_q, L::B_Q, s * 64, r0, bh);
-        load(sb + L::OFF_Q + L::TILE_BYTES + s * L::SLAB, &tm_q, L::B_Q, s * 64,
-             has1 ? qt1.row0 : p.nq, bh);
+        tma_load_3d(sb + L::OFF_Q + s * L::SLAB, &tm_q, bar(L::B_Q), s * 64, qt0.row0, bh);
+        // an absent second tile loads out of bounds (zero fill), never read
+        tma_load_3d(sb + L::OFF_Q + L::TILE_BYTES + s * L::SLAB, &tm_q, bar(L::B_Q), s * 64,
+                    has1 ? qt1.row0 : p.nq, bh);
       }
       TileCursor cur;
       cur.start(kr, rot);
       int ks = 0, kph = 0, vs = 0, vph = 0;
       for (int j = 0; j < n_tiles; ++j, cur.next(kr)) {
         const int krow = cur.row0(p.k_map);
-        wait_bar(L::B_KEMPTY + ks, kph ^ 1);
+        mbar_wait_sleep(bar(L::B_KEMPTY + ks), kph ^ 1);
         TR(45, j);
-        if (rank == 0) mbar_expect_tx(bar(L::B_KFULL + ks), NCTA * L::K_BYTES);
+        mbar_expect_tx(bar(L::B_KFULL + ks), L::TILE_BYTES);
         for (int s = 0; s < L::SLABS; ++s)
-          load(sb + L::OFF_K + ks * L::K_BYTES + s * L::KSLAB, &tm_k, L::B_KFULL + ks, s * 64,
-               krow + int(rank) * L::KROWS, bh_kv);
+          tma_load_3d(sb + L::OFF_K + ks * L::TILE_BYTES + s * L::SLAB, &tm_k,
+                      bar(L::B_KFULL + ks), s * 64, krow, bh_kv);
         if (++ks == L::KST) { ks = 0; kph ^= 1; }
-        wait_bar(L::B_VEMPTY + vs, vph ^ 1);
+        mbar_wait_sleep(bar(L::B_VEMPTY + vs), vph ^ 1);
         TR(46, j);
-        if (rank == 0) mbar_expect_tx(bar(L::B_VFULL + vs), NCTA * L::V_BYTES);
-        if constexpr (PAIR) {  // this CTA's 64 head dims of all 128 keys
-          load(sb + L::OFF_V + vs * L::V_BYTES, &tm_v, L::B_VFULL + vs, int(rank) * 64, krow,
-               bh_kv);
-        } else {
-          for (int s = 0; s < L::SLABS; ++s)
-            load(sb + L::OFF_V + vs * L::V_BYTES + s * L::SLAB, &tm_v, L::B_VFULL + vs, s * 64,
-                 krow, bh_kv);
-        }
+        mbar_expect_tx(bar(L::B_VFULL + vs), L::TILE_BYTES);
+        for (int s = 0; s < L::SLABS; ++s)
+          tma_load_3d(sb + L::OFF_V + vs * L::TILE_BYTES + s * L::SLAB, &tm_v,
+                      bar(L::B_VFULL + vs), s * 64, krow, bh_kv);
         if (++vs == L::VST) { vs = 0; vph ^= 1; }
       }
-    } else if (warp == 1 && n_tiles > 0 && rank == 0) {
+    } else if (warp == 1 && n_tiles > 0) {
       // -------------------------------------------------------- MMA issuer (whole warp, one elected lane issues)
       // head dims below the tile width: only ceil(h/16) K steps for Q K^T and
       // an N = 16 ceil(h/16) PV (the tile's other columns are zero fill)
-      // (PAIR: N = 128 always; the split of V's head dims is fixed at 64)
       const int ksteps = (p.h + 15) / 16;
-      constexpr int MM = PAIR ? 256 : 128;
-      constexpr uint32_t idesc_qk = make_idesc_bf16(MM, 128, 0, 0);
-      const uint32_t idesc_pv = make_idesc_bf16(MM, PAIR ? 128 : ksteps * 16, 0, 1);
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
+      const uint32_t idesc_pv = make_idesc_bf16(128, ksteps * 16, 0, 1);
       int ks = 0, kph = 0, vs = 0, vph = 0;
-      wait_bar(L::B_Q, 0);
+      mbar_wait_sleep(bar(L::B_Q), 0);
       // Descriptors are built once; per MMA only a constant is added to the
       // start-address field (16-byte units, no carry: shared memory < 256 KB),
       // so the issue loop keeps pace with the 64-cycle N=128 MMA even while
@@ -324,51 +271,38 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       const uint64_t dq0 = make_sdesc(sb + L::OFF_Q, 16, 1024);
       const uint64_t dk0 = make_sdesc(sb + L::OFF_K, 16, 1024);
       const uint64_t dv0 = make_sdesc(sb + L::OFF_V, L::SLAB, 1024);
-      auto mma_ss = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-        if constexpr (PAIR) umma_bf16_pair(d, a, b, id, acc);
-        else umma_bf16(d, a, b, id, acc);
-      };
-      auto mma_ts = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
-        if constexpr (PAIR) umma_bf16_ts_pair(d, a, b, id, acc);
-        else umma_bf16_ts(d, a, b, id, acc);
-      };
-      auto commit1 = [&](int b) {  // elected lane only
-        if constexpr (PAIR) umma_commit_pair(bar(b));
-        else umma_commit(bar(b));
-      };
       auto issue_qk = [&](int t) {  // S_t = Q_t K^T on the current K stage
         const uint64_t dq = dq0 + uint64_t(t * (L::TILE_BYTES >> 4));
-        const uint64_t dk = dk0 + uint64_t(ks * (L::K_BYTES >> 4));
+        const uint64_t dk = dk0 + uint64_t(ks * (L::TILE_BYTES >> 4));
         const uint32_t d = tmem + t * 128;
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint64_t qo = uint64_t(((kk >> 2) * L::SLAB + (kk & 3) * 32) >> 4);
-            const uint64_t ko = uint64_t(((kk >> 2) * L::KSLAB + (kk & 3) * 32) >> 4);
-            if (kk < ksteps) mma_ss(d, dq + qo, dk + ko, idesc_qk, kk > 0);
+            const uint64_t off = uint64_t(((kk >> 2) * L::SLAB + (kk & 3) * 32) >> 4);
+            if (kk < ksteps) umma_bf16(d, dq + off, dk + off, idesc_qk, kk > 0);
           }
-          commit1(L::B_SFULL + t);
+          umma_commit(bar(L::B_SFULL + t));
         }
         __syncwarp();
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P_t V on the current V stage
-        const uint64_t dv = dv0 + uint64_t(vs * (L::V_BYTES >> 4));
+        const uint64_t dv = dv0 + uint64_t(vs * (L::TILE_BYTES >> 4));
         const uint32_t pcol = tmem + t * 128;
         const uint32_t ocol = tmem + (t ? TM_O1 : TM_O0);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < TILE / 16; ++kk)
-            mma_ts(ocol, pcol + kk * 8, dv + uint64_t(kk * (2048 >> 4)), idesc_pv,
-                   (j > 0 || kk > 0) ? 1u : 0u);
+            umma_bf16_ts(ocol, pcol + kk * 8, dv + uint64_t(kk * (2048 >> 4)), idesc_pv,
+                         (j > 0 || kk > 0) ? 1u : 0u);
         }
         __syncwarp();
       };
       auto commit = [&](int b) {
-        if (elect_one()) commit1(b);
+        if (elect_one()) umma_commit(bar(b));
         __syncwarp();
       };
       // prologue: S0(0), S1(0)
-      wait_bar(L::B_KFULL + ks, kph);
+      mbar_wait_sleep(bar(L::B_KFULL + ks), kph);
       tc_fence_after();
       issue_qk(0);
       issue_qk(1);
@@ -376,15 +310,15 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       if (++ks == L::KST) { ks = 0; kph ^= 1; }
       for (int j = 0; j < n_tiles; ++j) {
         const bool more = j + 1 < n_tiles;
-        wait_bar(L::B_VFULL + vs, vph);
+        mbar_wait_sleep(bar(L::B_VFULL + vs), vph);
         TR(44, j);
         // ---- tile 0: PV0(j), QK0(j+1)
-        wait_bar(L::B_PFULL + 0, j & 1);
+        mbar_wait_sleep(bar(L::B_PFULL + 0), j & 1);
         tc_fence_after();
         TR(40, j);
         issue_pv(0, j);
         if (more) {
-          wait_bar(L::B_KFULL + ks, kph);
+          mbar_wait_sleep(bar(L::B_KFULL + ks), kph);
           tc_fence_after();
           issue_qk(0);
           TR(41, j);
@@ -392,7 +326,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
           commit(L::B_ODONE + 0);
         }
         // ---- tile 1: PV1(j), QK1(j+1)
-        wait_bar(L::B_PFULL + 1, j & 1);
+        mbar_wait_sleep(bar(L::B_PFULL + 1), j & 1);
         tc_fence_after();
         TR(42, j);
         issue_pv(1, j);
@@ -427,7 +361,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     if (arr) cur.start(kr, rot);
     const uint32_t s_addr = tmem + lane_addr + t * 128;
     const uint32_t o_addr = tmem + lane_addr + (t ? TM_O1 : TM_O0);
-    const bool present = t == 0 ? has0 : has1;
+    const bool present = (t == 0) || has1;
     const TileRef qt = t ? qt1 : qt0;
     for (int j = 0; j < n_tiles; ++j) {
       // Per-tile mask classes for affine maps are computed 32 tiles at a
@@ -463,8 +397,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
           lim = causal ? min(row - (int(inf & 0xffff) - 512), kvalid - 1) : kvalid - 1;
         }
       }
-      if constexpr (PAIR) mbar_wait_cluster(bar(L::B_SFULL + t), j & 1);
-      else mbar_wait(bar(L::B_SFULL + t), j & 1);
+      mbar_wait(bar(L::B_SFULL + t), j & 1);
       tc_fence_after();
       TR(0 * 8 + t * 4 + quarter, j);
       float s[NC];
@@ -559,17 +492,11 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       tmem_wait_st();
       tc_fence_before();
       TR(4 * 8 + t * 4 + quarter, j);
-      if (rank == 0) {
-        mbar_arrive(bar(L::B_PFULL + t));
-      } else {  // the peer's P reaches the leader's MMA: one arrival per warp
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_shared(bar(L::B_PFULL + t), 0));
-      }
+      mbar_arrive(bar(L::B_PFULL + t));
     }
     // ------------------------------------------------------------ epilogue
     if (n_tiles > 0) {
-      if constexpr (PAIR) mbar_wait_cluster(bar(L::B_ODONE + t), 0);
-      else mbar_wait(bar(L::B_ODONE + t), 0);
+      mbar_wait(bar(L::B_ODONE + t), 0);
       tc_fence_after();
     }
     if (present)
@@ -579,25 +506,23 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR) cluster_sync();  // no peer arrivals / MMAs in flight past this point
   if (warp == 1) {
     tc_fence_after();
-    if constexpr (PAIR) tmem_dealloc_pair(tmem, TMEM_COLS);
-    else tmem_dealloc(tmem, TMEM_COLS);
+    tmem_dealloc(tmem, TMEM_COLS);
   }
 }
 
 }  // namespace
 
-template <int HD, bool PAIR>
+template <int HD>
 int launch_fwd2_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                    const CUtensorMap& tv, cudaStream_t stream) {
-  using L = F2Layout<HD, PAIR>;
+  using L = F2Layout<HD>;
   static bool configured[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!configured[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(fwd2_kernel<HD, PAIR>,
+    cudaError_t e = cudaFuncSetAttribute(fwd2_kernel<HD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fwd2)");
     configured[dev & 63] = true;
@@ -605,43 +530,16 @@ int launch_fwd2_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUte
   const int q_tiles = (a.q_map.mode == A2D_IDX_AFFINE && a.q_map.nblocks > 1)
                           ? a.q_map.nblocks * (a.q_map.rows_per_block / TILE)
                           : (a.nq + TILE - 1) / TILE;
-  const int pairs = (q_tiles + 1) / 2;
-  if constexpr (!PAIR) {
-    dim3 grid(pairs, a.bh);
-    fwd2_kernel<HD, false><<<grid, F2_THREADS, L::SMEM, stream>>>(tq, tk, tv, a, q_tiles);
-    return check_launch("fwd2_kernel");
-  } else {
-    // keys staged 64 rows per CTA: a map with a 64-row box
-    CUtensorMap tk64;
-    const int g = a.kv_group > 1 ? a.kv_group : 1;
-    int rc = make_map_bf16(&tk64, a.k, a.h, a.nk, a.bh / g, a.k_stride_row, a.k_stride_bh, "k",
-                           L::KROWS);
-    if (rc) return rc;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * ((pairs + 1) / 2), a.bh);
-    cfg.blockDim = dim3(F2_THREADS);
-    cfg.dynamicSmemBytes = L::SMEM;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fwd2_kernel<HD, true>, tq, tk64, tv, a, q_tiles);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaLaunchKernelEx(fwd2 pair)");
-    return check_launch("fwd2_kernel (pair)");
-  }
+  dim3 grid((q_tiles + 1) / 2, a.bh);
+  fwd2_kernel<HD><<<grid, F2_THREADS, L::SMEM, stream>>>(tq, tk, tv, a, q_tiles);
+  return check_launch("fwd2_kernel");
 }
 
 int launch_tile_fwd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, cudaStream_t stream) {
-  // tiles are 64 or 128 columns wide; columns past h are TMA zero fill.
-  // 128-wide tiles run on CTA pairs (the 64-wide tile cannot split its V
-  // head dims into two 64-column halves)
-  if (a.h > 64) return launch_fwd2_hd<128, kFwdPair>(a, tq, tk, tv, stream);
-  return launch_fwd2_hd<64, false>(a, tq, tk, tv, stream);
+  // tiles are 64 or 128 columns wide; columns past h are TMA zero fill
+  if (a.h > 64) return launch_fwd2_hd<128>(a, tq, tk, tv, stream);
+  return launch_fwd2_hd<64>(a, tq, tk, tv, stream);
 }
 
 }  // namespace a2d

@@ -68,8 +68,6 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
     # no dQ drain work at all besides reading TMEM (wrong results): SMEM bound test
     "nodqsts": [(B, "for (int r = 0; r < DQ_ROUNDS; ++r, ++round) {", "for (int r = 0; r < 0; ++r, ++round) {")],
     "dqredT": [(B, "constexpr bool kDqRed = false;", "constexpr bool kDqRed = true;")],
-    # forward on single CTAs (no cta_group::2 pairs)
-    "fwd1": [(F, "constexpr bool kFwdPair = true;", "constexpr bool kFwdPair = false;")],
     "poly38": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)",
                 "#define B_POLY(c) ((((c) >> 1) & 7) == 1 || (((c) >> 1) & 7) == 4 || (((c) >> 1) & 7) == 6)")],
 }

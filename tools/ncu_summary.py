@@ -3,6 +3,7 @@ counters of `ncu --set full` reports (read here, without a GPU).
 
 usage: python tools/ncu_summary.py launches <launches.csv>
        python tools/ncu_summary.py report <x.ncu-rep> [algorithmic_flops_or_bytes] [unit]
+       python tools/ncu_summary.py traffic <fwd.ncu-rep> <bwd.ncu-rep> <config> <commit> > profiles/traffic.json
 """
 import csv
 import io
@@ -17,8 +18,14 @@ KEYS = [
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("lts__t_bytes.sum", "L2 bytes"),
-    ("TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
-     "tensor (hmma) cycles active, realtime avg per SM"),
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+     "tensor pipe active % of elapsed (tcgen05 utilisation)"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+     "shared-memory wavefronts to the tensor cores % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+     "shared-memory LSU wavefronts % of peak"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("dram__bytes.sum.per_second", "DRAM bandwidth"),
     ("sm__cycles_elapsed.avg", "SM cycles elapsed avg"),
     ("smsp__inst_executed.sum", "instructions"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
@@ -75,8 +82,38 @@ def report(path, algo=None, unit=None):
         print()
 
 
+def _raw(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return dict(zip(rows[0], rows[1])), [dict(zip(rows[0], r)) for r in rows[2:]]
+
+
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def traffic(fwd, bwd, config, commit):
+    """DRAM bytes per launch (read + write) of the last captured launch of
+    each report, for bench.py's roofline.traffic."""
+    import json
+    out = {"config": config, "source": f"ncu --set full --clock-control none, one launch each "
+                                        f"(tools/perf_tile.py at {config}), commit {commit}"}
+    for tag, path in (("tile_fwd", fwd), ("tile_bwd", bwd)):
+        units, rows = _raw(path)
+        r = rows[-1]
+        total = sum(float(r[k]) * SCALE.get(units[k], 1)
+                    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        out[f"{tag}_bytes_per_launch"] = int(total)
+        k = "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"
+        if k in r:
+            out[f"{tag}_tensor_pipe_pct"] = float(r[k])
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "traffic":
+        traffic(*sys.argv[2:6])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2])
     else:
         report(sys.argv[2], *(sys.argv[3:5]))
