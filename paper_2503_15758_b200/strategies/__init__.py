@@ -31,7 +31,7 @@ from .attn2d_no import Attention2D, Saved2D, attention2d
 from .attn2d_o import Attention2DO
 from .comm import GridComm
 from .common import DistAttnConfig, StrategyBackward, StrategyForward, assemble_rows
-from .relayout import from_cyclic, to_cyclic
+from .relayout import cyclic_token_ids, from_cyclic, shard_tokens, to_cyclic, unshard_tokens
 from .ring import RingAttention
 
 STRATEGY_NAMES = ("ring", "attn2d_no", "attn2d_o")
@@ -149,4 +149,5 @@ def run_backward(name: str, cfg: DistAttnConfig, saved, d_out) -> StrategyBackwa
 
 __all__ = ["STRATEGY_NAMES", "Attention2D", "Attention2DO", "DistAttnConfig", "GridComm", "RingAttention",
            "Saved2D", "StrategyBackward", "StrategyForward", "attention2d", "get_strategy",
-           "run_backward", "run_forward", "to_cyclic", "from_cyclic"]
+           "run_backward", "run_forward", "to_cyclic", "from_cyclic", "cyclic_token_ids",
+           "shard_tokens", "unshard_tokens"]
