@@ -10,6 +10,7 @@ that is not found aborts the build.  xlib2/ is scratch (git-ignored).
 
 from __future__ import annotations
 
+import os
 import shutil
 import subprocess
 import sys
@@ -67,7 +68,10 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
     ],
     # no dQ drain work at all besides reading TMEM (wrong results): SMEM bound test
     "nodqsts": [(B, "for (int r = 0; r < DQ_ROUNDS; ++r, ++round) {", "for (int r = 0; r < 0; ++r, ++round) {")],
-    "dqredT": [(B, "constexpr bool kDqRed = false;", "constexpr bool kDqRed = true;")],
+    "dqredT": [(B, "constexpr int kDqRedRounds = 0;", "constexpr int kDqRedRounds = 8;")],
+    "red1": [(B, "constexpr int kDqRedRounds = 0;", "constexpr int kDqRedRounds = 1;")],
+    "red2": [(B, "constexpr int kDqRedRounds = 0;", "constexpr int kDqRedRounds = 2;")],
+    "red3": [(B, "constexpr int kDqRedRounds = 0;", "constexpr int kDqRedRounds = 3;")],
     "poly38": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)",
                 "#define B_POLY(c) ((((c) >> 1) & 7) == 1 || (((c) >> 1) & 7) == 4 || (((c) >> 1) & 7) == 6)")],
 }
@@ -80,6 +84,18 @@ def build(name: str) -> Path:
         shutil.rmtree(work)
     shutil.copytree(CSRC, work / "pkg" / "csrc", ignore=shutil.ignore_patterns("build"))
     shutil.copytree(ROOT / "include", work / "include")
+    rev = os.environ.get("REV")  # sources of a git revision instead of the work tree
+    if rev:
+        for f in (work / "pkg" / "csrc").iterdir():
+            if f.is_file():
+                rel = f"paper_2503_15758_b200/csrc/{f.name}"
+                out = subprocess.run(["git", "show", f"{rev}:{rel}"], cwd=ROOT,
+                                     capture_output=True)
+                if out.returncode == 0:
+                    f.write_bytes(out.stdout)
+        hdr = subprocess.run(["git", "show", f"{rev}:include/attn2d_b200.h"], cwd=ROOT,
+                             capture_output=True, check=True).stdout
+        (work / "include" / "attn2d_b200.h").write_bytes(hdr)
     for fname, old, new in patches:
         p = work / "pkg" / "csrc" / fname
         s = p.read_text()
@@ -87,7 +103,7 @@ def build(name: str) -> Path:
             raise SystemExit(f"{name}: patch target not found in {fname}: {old[:60]!r}")
         p.write_text(s.replace(old, new))
     OUT.mkdir(exist_ok=True)
-    lib = OUT / f"lib_{name}.so"
+    lib = OUT / f"lib_{name}{os.environ.get('SUFFIX', '')}.so"
     mk = work / "pkg" / "csrc" / "Makefile"
     mk.write_text(mk.read_text().replace("LIB := ../libattn2d_b200.so", f"LIB := {lib}"))
     subprocess.run(["make", "-C", str(work / "pkg" / "csrc"), "-j8", "-s"], check=True)
