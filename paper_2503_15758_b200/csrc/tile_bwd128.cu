@@ -48,13 +48,12 @@ constexpr int OFF_Q = OFF_V + TILE_B;      // 2 stages
 constexpr int OFF_DO = OFF_Q + 2 * TILE_B;
 constexpr int OFF_DS = OFF_DO + TILE_B;
 // dQ staging: DQ_BUFS buffers of DQ_ROWS query rows x 128 fp32 (32 KB in all),
-// so up to DQ_BUFS TMA bulk reduce-adds are in flight per CTA.  The per-SM
-// bulk-reduce throughput (~20 B/clk measured) is what bounds this kernel:
-// 4 x 16-row buffers measured 1-3% faster than 2 x 32, 8 x 8 16% slower, and
-// moving rows to red.global.add from registers is slower still.
-// dQ rounds (of DQ_ROUNDS per tile) reduced from registers instead of
-// through shared memory
-constexpr int kDqRedRounds = 0;
+// so up to DQ_BUFS TMA bulk reduce-adds are in flight per CTA.  The staging
+// stores and the reduce's reads are a quarter of this kernel's shared-memory
+// traffic, which is what bounds it: 4 x 16-row buffers
+// measured 1-3% faster than 2 x 32, 8 x 8 16% slower; sending any share of
+// the rows by red.global.add.v4 from registers instead (scalar, vector,
+// coalesced through lane-quad transposes) measured 11-64% slower.
 constexpr int DQ_BUFS = 4;
 constexpr int DQ_ROWS = 64 / DQ_BUFS;
 constexpr int DQ_ROUNDS = 128 / DQ_ROWS;
@@ -488,38 +487,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(bar(B_DQFREE));
-      // Rounds [0, DQ_ROUNDS - kDqRedRounds) stage 16 query rows in shared
-      // memory and leave by TMA bulk reduce-add; the last kDqRedRounds go
-      // straight from registers by red.global.add.v4.f32 after 4 x 4
-      // transposes inside lane quads (each instruction covers four 128-byte
-      // row segments), trading shared-memory traffic for L2 atomics.
-      const TileRef qtl = tile_ref(p.q_map, p.nq, qrow);
 #pragma unroll
       for (int r = 0; r < DQ_ROUNDS; ++r) {
-        if (r >= DQ_ROUNDS - kDqRedRounds) {
-          const int m = lane & 3;
-          const bool b1 = (m & 2) != 0, b0 = (m & 1) != 0;
-          const int hh = quarter * 32 + (lane & ~3);  // first of this lane's 4 head dims
-          float* base = p.dq_acc + (long long)bh * p.dq_stride_bh + hh;
-#pragma unroll
-          for (int g = 0; g < DQ_ROWS / 4; ++g) {
-            const int q0 = DQ_ROWS * r + 4 * g;
-            const float a0 = v[q0], a1 = v[q0 + 1], a2 = v[q0 + 2], a3 = v[q0 + 3];
-            const float s0 = __shfl_xor_sync(0xffffffffu, b1 ? a0 : a2, 2);
-            const float s1 = __shfl_xor_sync(0xffffffffu, b1 ? a1 : a3, 2);
-            const float c0 = b1 ? s0 : a0, c1 = b1 ? s1 : a1, c2 = b1 ? a2 : s0, c3 = b1 ? a3 : s1;
-            const float t0 = __shfl_xor_sync(0xffffffffu, b0 ? c0 : c1, 1);
-            const float t1 = __shfl_xor_sync(0xffffffffu, b0 ? c2 : c3, 1);
-            const float d0 = b0 ? t0 : c0, d1 = b0 ? c1 : t0, d2 = b0 ? t1 : c2, d3 = b0 ? c3 : t1;
-            const int qq = q0 + m;
-            if (qq < qtl.nvalid && hh < p.h)
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
-                               base + (long long)(qrow + qq) * p.dq_stride_row),
-                           "f"(d0), "f"(d1), "f"(d2), "f"(d3)
-                           : "memory");
-          }
-          continue;
-        }
         const uint32_t buf = sb + OFF_DQ + (round % DQ_BUFS) * DQ_BUF_BYTES;
         ++round;
         // this buffer's previous reduce has read it
@@ -538,7 +507,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           bulk_commit_group();
         }
       }
-      (void)qtl;
     }
     if (h == 0) bulk_wait_group_all();
   }

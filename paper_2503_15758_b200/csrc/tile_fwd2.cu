@@ -401,30 +401,29 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       tc_fence_after();
       TR(0 * 8 + t * 4 + quarter, j);
       float s[NC];
-      auto mask_cols = [&](int j0, int j1) {  // causal / ragged columns -> -inf
-        if (partial) {
-#pragma unroll
-          for (int jj = j0; jj < j1; ++jj)
-            if (jj > lim) s[jj] = -INFINITY;
-        }
-      };
-      auto load_s = [&]() {  // S_t(j) row from TMEM
+      auto load_s = [&]() {  // S_t(j) row from TMEM, causal / ragged columns masked
 #pragma unroll
         for (int c = 0; c < NC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
         tmem_wait_ld();
-        mask_cols(0, NC);
+        if (partial) {
+#pragma unroll
+          for (int jj = 0; jj < NC; ++jj)
+            if (jj > lim) s[jj] = -INFINITY;
+        }
       };
+      load_s();
+      TR(1 * 8 + t * 4 + quarter, j);
       float alpha = 1.f;
       uint32_t pk[NC / 2];
       const float2 sc = make_float2(sl2, sl2);
-      // exponentials of columns [j0, j1) against the running max (P in pk,
-      // returns their share of the denominator)
-      auto exps = [&](float mbase, int j0, int j1) -> float {
+      // exponentials of this tile against the running max (P in pk, returns
+      // the tile's share of the denominator)
+      auto exps = [&](float mbase) -> float {
         float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
         const float2 nb = make_float2(-mbase, -mbase);
         if (partial) {  // masked entries are -inf: the exact MUFU path keeps them 0
 #pragma unroll
-          for (int jj = j0; jj < j1; jj += 2) {
+          for (int jj = 0; jj < NC; jj += 2) {
             const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
             const float2 e = make_float2(ex2(x.x), ex2(x.y));
             acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
@@ -432,7 +431,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
           }
         } else {  // some exponentials on the FMA pipe (MUFU offload, F2_POLY)
 #pragma unroll
-          for (int jj = j0; jj < j1; jj += 2) {
+          for (int jj = 0; jj < NC; jj += 2) {
             const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
             float2 e;
             if (F2_POLY(jj)) e = exp2_poly2(x);
@@ -450,33 +449,15 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       // (relative precision), so the max only has to move when a tile's sum
       // nears overflow (>= 2^64, or non-finite) — then it is recomputed
       // exactly and the tile redone.
-      float tsum;
-      if (__any_sync(0xffffffffu, m_run == -INFINITY)) {  // first visible tile: max of S
-        load_s();
-        TR(1 * 8 + t * 4 + quarter, j);
+      if (__any_sync(0xffffffffu, m_run == -INFINITY)) {
         const float m_new = fmaxf(m_run, rowmax<NC>(s) * sl2);
         if (m_new > m_run) {
           alpha = (m_run == -INFINITY) ? 1.f : ex2(m_run - m_new);
           m_run = m_new;
         }
-        TR(2 * 8 + t * 4 + quarter, j);
-        tsum = exps(m_run == -INFINITY ? 0.f : m_run, 0, NC);
-      } else {
-        // steady state: the second half of the S row streams out of TMEM
-        // while the first half's exponentials run
-#pragma unroll
-        for (int c = 0; c < NC / 64; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = NC / 64; c < NC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
-        TR(1 * 8 + t * 4 + quarter, j);
-        TR(2 * 8 + t * 4 + quarter, j);
-        mask_cols(0, NC / 2);
-        tsum = exps(m_run, 0, NC / 2);
-        tmem_wait_ld();
-        mask_cols(NC / 2, NC);
-        tsum += exps(m_run, NC / 2, NC);
       }
+      TR(2 * 8 + t * 4 + quarter, j);
+      float tsum = exps(m_run == -INFINITY ? 0.f : m_run);
       if (__any_sync(0xffffffffu, !(tsum < 0x1p64f))) {  // rare: S is still in TMEM
         load_s();
         const float m_new = fmaxf(m_run, rowmax<NC>(s) * sl2);
@@ -484,7 +465,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
           alpha *= (m_run == -INFINITY) ? 1.f : ex2(m_run - m_new);
           m_run = m_new;
         }
-        tsum = exps(m_run == -INFINITY ? 0.f : m_run, 0, NC);
+        tsum = exps(m_run == -INFINITY ? 0.f : m_run);
       }
       // Every tile adds less than 2^64 (else it was re-based above, after
       // which its entries are <= 1), so l_run < 2^64 * n_tiles <= 2^88 for

@@ -68,10 +68,6 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
     ],
     # no dQ drain work at all besides reading TMEM (wrong results): SMEM bound test
     "nodqsts": [(B, "for (int r = 0; r < DQ_ROUNDS; ++r, ++round) {", "for (int r = 0; r < 0; ++r, ++round) {")],
-    "dqredT": [(B, "constexpr int kDqRedRounds = 0;", "constexpr int kDqRedRounds = 8;")],
-    "red1": [(B, "constexpr int kDqRedRounds = 0;", "constexpr int kDqRedRounds = 1;")],
-    "red2": [(B, "constexpr int kDqRedRounds = 0;", "constexpr int kDqRedRounds = 2;")],
-    "red3": [(B, "constexpr int kDqRedRounds = 0;", "constexpr int kDqRedRounds = 3;")],
     "poly38": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)",
                 "#define B_POLY(c) ((((c) >> 1) & 7) == 1 || (((c) >> 1) & 7) == 4 || (((c) >> 1) & 7) == 6)")],
 }
