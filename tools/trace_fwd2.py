@@ -1,5 +1,6 @@
-"""Timeline of one fwd2 CTA from a -DF2X_TRACE build (diagnostic).
-usage: A2D_LIB_PATH=xlib/lib_trace.so python tools/trace_fwd2.py N BH causal"""
+"""Timeline of one fwd2 CTA from an A2D_TRACE build (diagnostic).
+usage: A2D_LIB_PATH=xlib2/lib_ftrace.so python tools/trace_fwd2.py N BH causal
+(build: python tools/mk_variant.py ftrace)"""
 import ctypes
 import sys
 from pathlib import Path
