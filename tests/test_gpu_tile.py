@@ -359,12 +359,13 @@ def test_other_head_dims(ops, h):
         assert rel_fro(got, want) < REL_TOL
 
 
+@pytest.mark.parametrize("h", [64, 128])
 @pytest.mark.parametrize("causal", [False, True])
-def test_forward_growing_scores_move_the_running_max(ops, causal):
+def test_forward_growing_scores_move_the_running_max(ops, causal, h):
     """Scores that grow by ~2^100 along the key sweep: the forward's running
     max (taken from the first visible tile, moved only when a tile's sum
     nears overflow) must re-base exactly; compared with the fp32 reference."""
-    bh, n, h = 2, 1024, 64
+    bh, n = 2, 1024
     g = torch.Generator(device="cpu").manual_seed(7)
     u = torch.randn((h,), generator=g)
     u = u / u.norm()
@@ -430,12 +431,14 @@ def test_full_size_row_and_key_sampled_parity(ops, n, bh):
     assert rel_fro(vg.grad[:, keys], dv_ref) < REL_TOL
 
 
-@pytest.mark.parametrize("col", [270, 271, 300])
-def test_forward_single_huge_score_on_any_column(ops, col):
+@pytest.mark.parametrize("h", [64, 128])
+@pytest.mark.parametrize("col", [270, 271, 300, 330, 383])
+def test_forward_single_huge_score_on_any_column(ops, col, h):
     """One key whose score exceeds every earlier tile's by ~2^200, placed on
     a column the forward evaluates with the FMA-pipe polynomial (270, 271)
-    or with MUFU (300): the overflow guard must catch it either way."""
-    bh, n, h = 1, 512, 64
+    or with MUFU (300, 330, 383), in either key half of its tile: the
+    overflow guard must catch it either way."""
+    bh, n = 1, 512
     g = torch.Generator(device="cpu").manual_seed(11)
     u = torch.randn((h,), generator=g)
     u = u / u.norm()
