@@ -70,6 +70,10 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
     "nodqsts": [(B, "for (int r = 0; r < DQ_ROUNDS; ++r, ++round) {", "for (int r = 0; r < 0; ++r, ++round) {")],
     # clock64 timeline of forward CTA (3, 5) for tools/trace_fwd2.py
     "ftrace": [(F, "// clock64 instrumentation points;", "#define A2D_TRACE 1\n#define TX 3\n#define TY 5\n// clock64 instrumentation points;")],
+    # backward: every mbarrier wait suspend-hinted instead of spinning
+    "bwdsleep": [(B, "#include \"kernels.h\"", "#include \"kernels.h\"\n#define mbar_wait mbar_wait_sleep")],
+    # forward: the softmax warps' S-ready waits suspend-hinted too
+    "fwdsleep": [(F, "#include \"kernels.h\"", "#include \"kernels.h\"\n#define mbar_wait mbar_wait_sleep")],
     "poly38": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)",
                 "#define B_POLY(c) ((((c) >> 1) & 7) == 1 || (((c) >> 1) & 7) == 4 || (((c) >> 1) & 7) == 6)")],
 }

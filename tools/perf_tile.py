@@ -9,7 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2503_15758_b200 import ops  # noqa: E402
 
 
-def timeit(fn, iters=5, warm=2):
+def timeit(fn, iters=int(__import__("os").environ.get("A2D_PERF_ITERS", "5")), warm=2):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
