@@ -27,7 +27,7 @@ def test_reference_arm_prints_one_contract_line():
 
 
 def test_gpu_line_in_profiles_has_the_contract_keys():
-    line = json.loads((ROOT / "profiles" / "r1_bench_1gpu.json").read_text().strip())
+    line = json.loads((ROOT / "profiles" / "r2_bench_1gpu.json").read_text().strip())
     for key in ("roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert key in line, key
     r = line["roofline"]
