@@ -453,3 +453,54 @@ def test_forward_single_huge_score_on_any_column(ops, col, h):
         assert torch.isfinite(o).all() and torch.isfinite(lse).all()
         assert rel_fro(o, want_o) < REL_TOL, (causal, rel_fro(o, want_o))
         assert max_abs(lse, want_lse) < 1e-3 * max(1.0, float(want_lse.abs().max()))
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_backward_accumulate_mode_adds_to_existing_dkv(ops, causal):
+    """accumulate_dkv (ABI v3): two key-disjoint query subsets accumulated
+    into one fp32 dK/dV buffer equal the full-query backward (the ring's and
+    attn2d_o's hop accumulation, reference ring.py:118-143)."""
+    bh, n, h = 2, 384, 128
+    scale = h ** -0.5
+    q, k, v, do = (uniform((bh, n, h), s) for s in (51, 52, 53, 54))
+    o, lse = ops.tile_forward(q, k, v, causal=causal, scale=scale, out_dtype=torch.bfloat16)
+    delta = ops.bwd_preprocess(o, do)
+    _, dk_full, dv_full = ops.tile_backward(q, k, v, do, lse, delta, causal=causal, scale=scale)
+    dk = torch.full((bh, n, h), 0.25, device="cuda")
+    dv = torch.full((bh, n, h), -0.5, device="cuda")
+    dk0, dv0 = dk.clone(), dv.clone()
+    for a, b in ((0, 128), (128, 384)):   # query row subsets (global positions a..b-1)
+        qi = ops.TokenIndex.contiguous(b - a, a)
+        dq_part = torch.zeros((bh, b - a, h), device="cuda")
+        ops.tile_backward(q[:, a:b].contiguous(), k, v, do[:, a:b].contiguous(),
+                          lse[:, a:b].contiguous(), delta[:, a:b].contiguous(), causal=causal,
+                          scale=scale, q_index=qi, dq_acc=dq_part, dk=dk, dv=dv,
+                          accumulate_dkv=True)
+    torch.cuda.synchronize()
+    assert rel_fro(dk - dk0, dk_full) < 1e-5
+    assert rel_fro(dv - dv0, dv_full) < 1e-5
+
+
+def test_backward_without_query_rows_writes_zero_dkv(ops):
+    """nq == 0: nothing attends these keys, dK / dV are zero (reference
+    attention.py:250-252), in both output dtypes."""
+    bh, nk, h = 2, 200, 64
+    k, v = uniform((bh, nk, h), 61), uniform((bh, nk, h), 62)
+    q = torch.empty((bh, 0, h), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((bh, 0), device="cuda")
+    for dt in (torch.float32, torch.bfloat16):
+        dk = torch.full((bh, nk, h), 7.0, dtype=dt, device="cuda")
+        dv = torch.full((bh, nk, h), 7.0, dtype=dt, device="cuda")
+        ops.tile_backward(q, k, v, q, lse, lse, causal=True, scale=0.125, dk=dk, dv=dv)
+        torch.cuda.synchronize()
+        assert bool((dk == 0).all()) and bool((dv == 0).all())
+
+
+def test_forward_without_heads_or_rows_is_a_no_op(ops):
+    """bh == 0 and nq == 0 launch nothing and succeed (a2d_tile_fwd)."""
+    for bh, nq in ((0, 128), (2, 0)):
+        q = torch.empty((bh, nq, 64), dtype=torch.bfloat16, device="cuda")
+        k = uniform((bh, 64, 64), 63) if bh else torch.empty((0, 64, 64), dtype=torch.bfloat16,
+                                                              device="cuda")
+        o, lse = ops.tile_forward(q, k, k, causal=True, scale=0.125)
+        assert o.shape == (bh, nq, 64) and lse.shape == (bh, nq)
