@@ -136,6 +136,8 @@ def launches() -> int:
 def _kv_group(bh: int, k: torch.Tensor) -> int:
     """Query heads per key/value head (GQA / MQA)."""
     bk = k.shape[0] if k.dim() == 3 else 0
+    if bh == 0 and bk == 0:
+        return 1
     if bk < 1 or bh % bk:
         raise ShapeError(f"{bk} key/value heads do not divide {bh} query heads")
     return bh // bk
