@@ -192,8 +192,8 @@ int a2d_tile_fwd(const a2d_tile_fwd_args* a, void* stream) {
     return set_error(A2D_EINVAL, "o_dtype invalid");
   if (a->accumulate && a->o_dtype != A2D_F32)
     return set_error(A2D_EINVAL, "accumulate requires an fp32 partial O");
+  if (a->bh == 0 || a->nq == 0) return A2D_OK;  // empty outputs may have null pointers
   if (!a->o || !a->lse) return set_error(A2D_EINVAL, "o / lse are null");
-  if (a->bh == 0 || a->nq == 0) return A2D_OK;
   if (a->nk == 0) {  // nothing to attend: the empty partial (attention.py:91-97)
     if (a->accumulate) return A2D_OK;
     return set_error(A2D_EINVAL, "nk == 0 without accumulate");
@@ -212,6 +212,8 @@ int a2d_bwd_preprocess(const void* o, const void* dout, float* delta, int64_t o_
                        int32_t bh, int32_t n, int32_t h, void* stream) {
   if (h < 8 || h > 128 || h % 8)
     return set_error(A2D_EUNSUPPORTED, "head dim %d not a multiple of 8 in [8, 128]", h);
+  if (bh < 0 || n < 0) return set_error(A2D_EINVAL, "negative sizes");
+  if (bh == 0 || n == 0) return A2D_OK;
   if (!o || !dout || !delta) return set_error(A2D_EINVAL, "null pointer");
   return launch_bwd_preprocess(o, dout, delta, o_stride_bh, o_stride_row, do_stride_bh,
                                do_stride_row, bh, n, h, static_cast<cudaStream_t>(stream));
@@ -225,12 +227,12 @@ int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
   if (a->kv_group < 0 || a->bh % g) return set_error(A2D_EINVAL, "kv_group %d must divide bh %d", a->kv_group, a->bh);
   if (a->dkv_dtype != A2D_F32 && a->dkv_dtype != A2D_BF16)
     return set_error(A2D_EINVAL, "dkv_dtype invalid");
+  if (a->accumulate_dkv && a->dkv_dtype != A2D_F32)
+    return set_error(A2D_EINVAL, "accumulate_dkv requires fp32 dk / dv");
+  if (a->bh == 0 || a->nk == 0) return A2D_OK;  // empty outputs may have null pointers
   if (!a->dk || !a->dv) return set_error(A2D_EINVAL, "null dk / dv pointer");
   if (a->nq > 0 && (!a->lse || !a->delta || !a->dq_acc))
     return set_error(A2D_EINVAL, "null dq_acc / statistics pointer");
-  if (a->accumulate_dkv && a->dkv_dtype != A2D_F32)
-    return set_error(A2D_EINVAL, "accumulate_dkv requires fp32 dk / dv");
-  if (a->bh == 0 || a->nk == 0) return A2D_OK;
   if (a->nq == 0) {  // no query rows: zero gradients (reference attention.py:250-252)
     if (a->accumulate_dkv) return A2D_OK;
     if ((a->dkv_stride_bh | a->dkv_stride_row) % 4)
@@ -257,6 +259,8 @@ int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
 int a2d_bwd_finalize(const float* dq_acc, int64_t acc_stride_bh, int64_t acc_stride_row, void* dq,
                      int32_t out_dtype, int64_t dq_stride_bh, int64_t dq_stride_row, int32_t bh,
                      int32_t n, int32_t h, float scale, void* stream) {
+  if (bh < 0 || n < 0) return set_error(A2D_EINVAL, "negative sizes");
+  if (bh == 0 || n == 0) return A2D_OK;
   if (!dq_acc || !dq) return set_error(A2D_EINVAL, "null pointer");
   if (h % 4 || acc_stride_bh % 4 || acc_stride_row % 4 || dq_stride_bh % 4 || dq_stride_row % 4)
     return set_error(A2D_EINVAL, "h and strides must be multiples of 4");
@@ -272,6 +276,8 @@ int a2d_lse_merge(const float* o_parts, const float* lse_parts, int32_t k_parts,
   if (k_parts < 1 || k_parts > 16) return set_error(A2D_EUNSUPPORTED, "k_parts must be in [1, 16]");
   if (h % 4 || row_stride % 4 || part_stride_o % 4)
     return set_error(A2D_EINVAL, "h and strides must be multiples of 4");
+  if (rows < 0) return set_error(A2D_EINVAL, "negative sizes");
+  if (rows == 0) return A2D_OK;
   if (!o_parts || !lse_parts || !o_out || !lse_out) return set_error(A2D_EINVAL, "null pointer");
   if (out_dtype != A2D_F32 && out_dtype != A2D_BF16) return set_error(A2D_EINVAL, "out_dtype invalid");
   return launch_lse_merge(o_parts, lse_parts, k_parts, part_stride_o, part_stride_lse, rows, h,

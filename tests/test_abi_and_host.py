@@ -161,3 +161,23 @@ def test_abi_argument_validation_without_a_gpu():
     a.kv_group, a.nq = 1, -1
     assert lib.a2d_tile_fwd(a, None) == _lib.A2D_EINVAL
     assert b"negative" in lib.a2d_last_error()
+
+
+def test_abi_empty_calls_succeed_with_null_buffers():
+    """Zero heads or zero rows is a valid call that touches no memory: empty
+    torch tensors carry null data pointers, so the null checks come after
+    the emptiness checks (no CUDA work, so this runs without a GPU)."""
+    lib = _lib.load()
+    a = _lib.TileFwdArgs()
+    a.nq, a.nk, a.h, a.causal, a.scale, a.o_dtype = 128, 128, 64, 1, 0.125, _lib.F32
+    for m in (a.q_map, a.k_map):
+        m.mode, m.nblocks, m.rows_per_block, m.stride = _lib.IDX_AFFINE, 1, 128, 1
+    a.bh = 0
+    assert lib.a2d_tile_fwd(a, None) == _lib.A2D_OK
+    a.bh, a.nq, a.q_map.rows_per_block = 2, 0, 0
+    assert lib.a2d_tile_fwd(a, None) == _lib.A2D_OK
+    assert lib.a2d_bwd_preprocess(None, None, None, 0, 0, 0, 0, 0, 128, 64, None) == _lib.A2D_OK
+    assert lib.a2d_bwd_finalize(None, 0, 0, None, _lib.F32, 0, 0, 2, 0, 64, 1.0, None) == _lib.A2D_OK
+    assert lib.a2d_lse_merge(None, None, 2, 0, 0, 0, 64, 64, None, _lib.F32, 64, None,
+                             None) == _lib.A2D_OK
+    assert lib.a2d_bwd_preprocess(None, None, None, 0, 0, 0, 0, -1, 128, 64, None) == _lib.A2D_EINVAL
