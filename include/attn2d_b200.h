@@ -23,6 +23,9 @@
  *       A2D_ECUDA = 3 (CUDA launch / runtime error).
  *     a2d_last_error() returns a thread-local message for the last failure.
  *   - tensors are [bh, rows, h] with unit stride along h; strides in elements.
+ *   - a call with no work (zero heads, or zero rows on the side that owns the
+ *     outputs' rows) returns A2D_OK before any pointer is checked or
+ *     dereferenced: empty framework tensors may carry null data pointers.
  *   - the partial state of one query row is (O, LSE): O normalised by its own
  *     denominator and LSE = m + log(d) (natural log, -inf for a row that has
  *     attended nothing).  This is the reference's (m, n, d) triple
