@@ -150,6 +150,16 @@ def _c1_reference_seconds(ref) -> float:
     return time.perf_counter() - t0
 
 
+def _cpu_model() -> str | None:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_sample(n_cpu=4096, h=128, causal=True, budget_s=12.0, max_heads=32, with_c1=True):
     """Time the reference algorithm on the host cores on a bounded sample of
     the metric workload: whole heads of N=n_cpu, causal fwd+bwd.  With the
@@ -185,7 +195,8 @@ def cpu_sample(n_cpu=4096, h=128, causal=True, budget_s=12.0, max_heads=32, with
     dt = time.perf_counter() - t0
     fl = 3.5 * flops_fwd(1, heads, h, n_cpu, causal)
     out = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": kind,
-           "seconds": dt,
+           "seconds": dt, "cpu_model": _cpu_model(),
+           "backend": "numpy" if ref is not None else "oracle (numpy)",
            "sample": f"{heads} head(s) of N={n_cpu}, H={h}, {'causal' if causal else 'non-causal'} "
                      f"fwd+bwd through {how}; BLAS threads = all host cores"}
     if ref is not None and with_c1:
