@@ -51,7 +51,7 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
         (B, "umma_bf16(tmem + TM_Y, kb + mofs(kk), dsb + mofs(kk), id_mnmn, kk > 0);",
             "umma_bf16(tmem + TM_Y, dsb + mofs(kk), kb + mofs(kk), id_mnmn, kk > 0);"),
         (B, """#pragma unroll
-      for (int r = 0; r < DQ_ROUNDS; ++r, ++round) {
+      for (int r = 0; r < DQ_ROUNDS; ++r) {
         const uint32_t buf = sb + OFF_DQ + (round % DQ_BUFS) * DQ_BUF_BYTES;""",
             """const TileRef qtl = tile_ref(p.q_map, p.nq, qrow);
       if (h < qtl.nvalid) {
@@ -63,11 +63,11 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
                          "f"(v[c]), "f"(v[c + 1]), "f"(v[c + 2]), "f"(v[c + 3]) : "memory");
       }
 #pragma unroll
-      for (int r = 0; r < 0; ++r, ++round) {
+      for (int r = 0; r < 0; ++r) {
         const uint32_t buf = sb + OFF_DQ + (round % DQ_BUFS) * DQ_BUF_BYTES;"""),
     ],
     # no dQ drain work at all besides reading TMEM (wrong results): SMEM bound test
-    "nodqsts": [(B, "for (int r = 0; r < DQ_ROUNDS; ++r, ++round) {", "for (int r = 0; r < 0; ++r, ++round) {")],
+    "nodqsts": [(B, "for (int r = 0; r < DQ_ROUNDS; ++r) {", "for (int r = 0; r < 0; ++r) {")],
     # clock64 timeline of forward CTA (3, 5) for tools/trace_fwd2.py
     "ftrace": [(F, "// clock64 instrumentation points;", "#define A2D_TRACE 1\n#define TX 3\n#define TY 5\n// clock64 instrumentation points;")],
     # backward: every mbarrier wait suspend-hinted instead of spinning
