@@ -40,12 +40,12 @@
 extern "C" {
 #endif
 
-#define A2D_ABI_VERSION 3
+#define A2D_ABI_VERSION 4
 #define A2D_MAX_BLOCKS 16
 
 enum { A2D_OK = 0, A2D_EINVAL = 1, A2D_EUNSUPPORTED = 2, A2D_ECUDA = 3 };
 enum { A2D_IDX_AFFINE = 0, A2D_IDX_ARRAY = 1 };
-enum { A2D_F32 = 0, A2D_BF16 = 1 };
+enum { A2D_F32 = 0, A2D_BF16 = 1, A2D_F16 = 2 };
 
 /* Global token index of every local row — the reference's TokenShard.indices
  * (attention.py:50-72) in a form the kernel can evaluate without memory
@@ -72,8 +72,10 @@ typedef struct {
 
 /* Tile forward: kernels.flash_forward (reference kernels/__init__.py:70-78,
  * numpy_backend.py:24-43) for bh independent heads.
- *   q [bh, nq, h], k/v [bh, nk, h] bf16.
- *   o [bh, nq, h] (o_dtype A2D_F32: normalised partial O; A2D_BF16: final O),
+ *   q [bh, nq, h], k/v [bh, nk, h]: in_dtype A2D_BF16 (0 reads as bf16) or
+ *   A2D_F16, all three alike.
+ *   o [bh, nq, h] (o_dtype A2D_F32: normalised partial O; A2D_BF16 or
+ *   A2D_F16: final O),
  *   lse [bh, nq] fp32 natural-log LSE (-inf: row attended nothing here).
  *   accumulate = 1 continues from the (o, lse) state already in the buffers
  *   (requires A2D_F32): the streaming continuation of the reference kernel
@@ -99,18 +101,19 @@ typedef struct {
   a2d_index_map q_map;
   a2d_index_map k_map;
   int32_t kv_group;
-  int32_t reserved2;
+  int32_t in_dtype;
 } a2d_tile_fwd_args;
 
 int a2d_tile_fwd(const a2d_tile_fwd_args* args, void* stream);
 
 /* delta[bh, n] = rowsum(dO * O) in fp32 — the first line of the reference's
  * backward recurrence (numpy_backend.py:49, numba_backend.py:84-86).
- * o, dout are bf16 [bh, n, h] with the given strides. */
+ * o, dout are [bh, n, h] of in_dtype (A2D_BF16 or A2D_F16) with the given
+ * strides. */
 int a2d_bwd_preprocess(const void* o, const void* dout, float* delta,
                        int64_t o_stride_bh, int64_t o_stride_row,
                        int64_t do_stride_bh, int64_t do_stride_row,
-                       int32_t bh, int32_t n, int32_t h, void* stream);
+                       int32_t bh, int32_t n, int32_t h, int32_t in_dtype, void* stream);
 
 /* Tile backward: kernels.flash_backward (kernels/__init__.py:81-92,
  * numpy_backend.py:46-62).  lse / delta are the GLOBAL row statistics of q's
@@ -118,7 +121,8 @@ int a2d_bwd_preprocess(const void* o, const void* dout, float* delta,
  * this key subset (attention.py:225-257).
  *   dq_acc [bh, nq, h] fp32 (strides dq_stride_*, multiples of 4 elements):
  *   dS K (unscaled) is ADDED to it with TMA reduce-add (caller zeroes);
- *   dk, dv [bh, nk, h]: written (dkv_dtype A2D_F32 or A2D_BF16); dk is
+ *   q, k, v, dout: in_dtype (A2D_BF16, 0 reads as bf16, or A2D_F16).
+ *   dk, dv [bh, nk, h]: written (dkv_dtype A2D_F32, A2D_BF16 or A2D_F16); dk is
  *   already multiplied by scale.  accumulate_dkv = 1 ADDS the contributions
  *   to the fp32 dk / dv already in the buffers instead (the ring's and the
  *   overlapped schedule's per-hop accumulation, reference ring.py:118-143).
@@ -149,13 +153,13 @@ typedef struct {
   a2d_index_map q_map;
   a2d_index_map k_map;
   int32_t kv_group;
-  int32_t reserved2;
+  int32_t in_dtype;
 } a2d_tile_bwd_args;
 
 int a2d_tile_bwd(const a2d_tile_bwd_args* args, void* stream);
 
-/* dq = scale * dq_acc, converted to out_dtype; both [bh, n, h] with the
- * given strides (unit stride along h). */
+/* dq = scale * dq_acc, converted to out_dtype (A2D_F32, A2D_BF16 or
+ * A2D_F16); both [bh, n, h] with the given strides (unit stride along h). */
 int a2d_bwd_finalize(const float* dq_acc, int64_t acc_stride_bh, int64_t acc_stride_row,
                      void* dq, int32_t out_dtype, int64_t dq_stride_bh, int64_t dq_stride_row,
                      int32_t bh, int32_t n, int32_t h, float scale, void* stream);
@@ -164,7 +168,8 @@ int a2d_bwd_finalize(const float* dq_acc, int64_t acc_stride_bh, int64_t acc_str
  * attn_fix folded over k parts (attention.py:194-214) fused with finalize
  * (attention.py:217-222).  Part i lives at o_parts + i*part_stride_o
  * (fp32 [rows, h] rows of `row_stride` elements) and
- * lse_parts + i*part_stride_lse.  Writes o_out (out_dtype, [rows, h] with
+ * lse_parts + i*part_stride_lse.  Writes o_out (out_dtype A2D_F32, A2D_BF16
+ * or A2D_F16, [rows, h] with
  * out_row_stride) and lse_out (fp32 [rows]); rows whose every part is empty
  * get O = 0 and LSE = -inf (the caller raises FullyMaskedRowError). */
 int a2d_lse_merge(const float* o_parts, const float* lse_parts, int32_t k_parts,

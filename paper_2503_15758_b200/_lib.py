@@ -16,12 +16,12 @@ from .errors import ShapeError, UnsupportedError
 
 LIB_PATH = Path(os.environ.get("A2D_LIB_PATH") or
                 Path(__file__).resolve().parent / "libattn2d_b200.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 MAX_BLOCKS = 16
 
 A2D_OK, A2D_EINVAL, A2D_EUNSUPPORTED, A2D_ECUDA = 0, 1, 2, 3
 IDX_AFFINE, IDX_ARRAY = 0, 1
-F32, BF16 = 0, 1
+F32, BF16, F16 = 0, 1, 2
 
 # every symbol include/attn2d_b200.h declares
 EXPORTS = ("a2d_tile_fwd", "a2d_bwd_preprocess", "a2d_tile_bwd", "a2d_bwd_finalize",
@@ -45,7 +45,7 @@ class TileFwdArgs(ctypes.Structure):
                 ("bh", c_int32), ("nq", c_int32), ("nk", c_int32), ("h", c_int32),
                 ("causal", c_int32), ("scale", c_float), ("o_dtype", c_int32),
                 ("accumulate", c_int32), ("q_map", IndexMap), ("k_map", IndexMap),
-                ("kv_group", c_int32), ("reserved2", c_int32)]
+                ("kv_group", c_int32), ("in_dtype", c_int32)]
 
 
 class TileBwdArgs(ctypes.Structure):
@@ -61,7 +61,7 @@ class TileBwdArgs(ctypes.Structure):
                 ("bh", c_int32), ("nq", c_int32), ("nk", c_int32), ("h", c_int32),
                 ("causal", c_int32), ("scale", c_float), ("dkv_dtype", c_int32),
                 ("accumulate_dkv", c_int32), ("q_map", IndexMap), ("k_map", IndexMap),
-                ("kv_group", c_int32), ("reserved2", c_int32)]
+                ("kv_group", c_int32), ("in_dtype", c_int32)]
 
 
 _LIB = None
@@ -81,7 +81,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     lib.a2d_tile_fwd.argtypes = [ctypes.POINTER(TileFwdArgs), c_void_p]
     lib.a2d_tile_bwd.argtypes = [ctypes.POINTER(TileBwdArgs), c_void_p]
     lib.a2d_bwd_preprocess.argtypes = [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
-                                       c_int64, c_int32, c_int32, c_int32, c_void_p]
+                                       c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p]
     lib.a2d_bwd_finalize.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64,
                                      c_int64, c_int32, c_int32, c_int32, c_float, c_void_p]
     lib.a2d_lse_merge.argtypes = [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int64,

@@ -56,7 +56,7 @@ EncodeTiledFn encode_fn() {
 // 3-D map over a bf16 [bh, rows, h] tensor (unit stride along h), box 64 x 128 x 1,
 // 128-byte swizzle: one box is one K-major SW128 slab of a 128-row tile.
 int make_map(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long long s_row,
-             long long s_bh, const char* name, int box_rows = 128) {
+             long long s_bh, const char* name, int box_rows = 128, bool f16 = false) {
   if (ptr == nullptr) return set_error(A2D_EINVAL, "%s is null", name);
   if (reinterpret_cast<uintptr_t>(ptr) % 16)
     return set_error(A2D_EINVAL, "%s must be 16-byte aligned", name);
@@ -69,7 +69,8 @@ int make_map(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long long
   if (bh == 1) strides[1] = (cuuint64_t)((long long)rows * s_row * 2);
   cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+  CUresult r = fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                  const_cast<void*>(ptr), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(A2D_ECUDA, "cuTensorMapEncodeTiled(%s) failed: %d", name, (int)r);
@@ -82,6 +83,16 @@ int make_map_bf16(CUtensorMap* m, const void* ptr, int h, int rows, int bh, long
                   long long s_bh, const char* name, int box_rows) {
   return make_map(m, ptr, h, rows, bh, s_row, s_bh, name, box_rows);
 }
+
+// 16-bit operand type of a tile call: 0 (the v3 reserved field) reads as bf16
+static int in_type(int32_t in_dtype, bool* f16) {
+  if (in_dtype != 0 && in_dtype != A2D_BF16 && in_dtype != A2D_F16)
+    return set_error(A2D_EUNSUPPORTED, "in_dtype %d: inputs must be bf16 or fp16", in_dtype);
+  *f16 = in_dtype == A2D_F16;
+  return A2D_OK;
+}
+
+static bool out16_ok(int32_t dt) { return dt == A2D_F32 || dt == A2D_BF16 || dt == A2D_F16; }
 
 // fp32 [bh, rows, h] contiguous accumulator, box 32 x box_rows x 1, 128B swizzle
 // (the backward's dQ reduce-add target).
@@ -188,8 +199,9 @@ int a2d_tile_fwd(const a2d_tile_fwd_args* a, void* stream) {
   if (rc) return rc;
   const int g = a->kv_group > 1 ? a->kv_group : 1;
   if (a->kv_group < 0 || a->bh % g) return set_error(A2D_EINVAL, "kv_group %d must divide bh %d", a->kv_group, a->bh);
-  if (a->o_dtype != A2D_F32 && a->o_dtype != A2D_BF16)
-    return set_error(A2D_EINVAL, "o_dtype invalid");
+  if (!out16_ok(a->o_dtype)) return set_error(A2D_EINVAL, "o_dtype invalid");
+  bool f16 = false;
+  if ((rc = in_type(a->in_dtype, &f16))) return rc;
   if (a->accumulate && a->o_dtype != A2D_F32)
     return set_error(A2D_EINVAL, "accumulate requires an fp32 partial O");
   if (a->bh == 0 || a->nq == 0) return A2D_OK;  // empty outputs may have null pointers
@@ -201,22 +213,30 @@ int a2d_tile_fwd(const a2d_tile_fwd_args* a, void* stream) {
   if (a->o_stride_row % 4 || a->o_stride_bh % 4)
     return set_error(A2D_EINVAL, "o strides must be multiples of 4 elements");
   CUtensorMap tq, tk, tv;
-  if ((rc = make_map(&tq, a->q, a->h, a->nq, a->bh, a->q_stride_row, a->q_stride_bh, "q"))) return rc;
-  if ((rc = make_map(&tk, a->k, a->h, a->nk, a->bh / g, a->k_stride_row, a->k_stride_bh, "k"))) return rc;
-  if ((rc = make_map(&tv, a->v, a->h, a->nk, a->bh / g, a->v_stride_row, a->v_stride_bh, "v"))) return rc;
+  if ((rc = make_map(&tq, a->q, a->h, a->nq, a->bh, a->q_stride_row, a->q_stride_bh, "q", 128, f16)))
+    return rc;
+  if ((rc = make_map(&tk, a->k, a->h, a->nk, a->bh / g, a->k_stride_row, a->k_stride_bh, "k", 128,
+                     f16)))
+    return rc;
+  if ((rc = make_map(&tv, a->v, a->h, a->nk, a->bh / g, a->v_stride_row, a->v_stride_bh, "v", 128,
+                     f16)))
+    return rc;
   return launch_tile_fwd(*a, tq, tk, tv, static_cast<cudaStream_t>(stream));
 }
 
 int a2d_bwd_preprocess(const void* o, const void* dout, float* delta, int64_t o_stride_bh,
                        int64_t o_stride_row, int64_t do_stride_bh, int64_t do_stride_row,
-                       int32_t bh, int32_t n, int32_t h, void* stream) {
+                       int32_t bh, int32_t n, int32_t h, int32_t in_dtype, void* stream) {
+  bool f16 = false;
+  int rc = in_type(in_dtype, &f16);
+  if (rc) return rc;
   if (h < 8 || h > 128 || h % 8)
     return set_error(A2D_EUNSUPPORTED, "head dim %d not a multiple of 8 in [8, 128]", h);
   if (bh < 0 || n < 0) return set_error(A2D_EINVAL, "negative sizes");
   if (bh == 0 || n == 0) return A2D_OK;
   if (!o || !dout || !delta) return set_error(A2D_EINVAL, "null pointer");
   return launch_bwd_preprocess(o, dout, delta, o_stride_bh, o_stride_row, do_stride_bh,
-                               do_stride_row, bh, n, h, static_cast<cudaStream_t>(stream));
+                               do_stride_row, bh, n, h, f16, static_cast<cudaStream_t>(stream));
 }
 
 int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
@@ -225,8 +245,9 @@ int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
   if (rc) return rc;
   const int g = a->kv_group > 1 ? a->kv_group : 1;
   if (a->kv_group < 0 || a->bh % g) return set_error(A2D_EINVAL, "kv_group %d must divide bh %d", a->kv_group, a->bh);
-  if (a->dkv_dtype != A2D_F32 && a->dkv_dtype != A2D_BF16)
-    return set_error(A2D_EINVAL, "dkv_dtype invalid");
+  if (!out16_ok(a->dkv_dtype)) return set_error(A2D_EINVAL, "dkv_dtype invalid");
+  bool f16 = false;
+  if ((rc = in_type(a->in_dtype, &f16))) return rc;
   if (a->accumulate_dkv && a->dkv_dtype != A2D_F32)
     return set_error(A2D_EINVAL, "accumulate_dkv requires fp32 dk / dv");
   if (a->bh == 0 || a->nk == 0) return A2D_OK;  // empty outputs may have null pointers
@@ -247,11 +268,17 @@ int a2d_tile_bwd(const a2d_tile_bwd_args* a, void* stream) {
   }
   CUtensorMap tq, tk, tv, tdo;
   const int qt = bwd_q_tile_rows(a->h);
-  if ((rc = make_map(&tq, a->q, a->h, a->nq, a->bh, a->q_stride_row, a->q_stride_bh, "q", qt))) return rc;
-  if ((rc = make_map(&tk, a->k, a->h, a->nk, a->bh / g, a->k_stride_row, a->k_stride_bh, "k"))) return rc;
-  if ((rc = make_map(&tv, a->v, a->h, a->nk, a->bh / g, a->v_stride_row, a->v_stride_bh, "v"))) return rc;
+  if ((rc = make_map(&tq, a->q, a->h, a->nq, a->bh, a->q_stride_row, a->q_stride_bh, "q", qt,
+                     f16)))
+    return rc;
+  if ((rc = make_map(&tk, a->k, a->h, a->nk, a->bh / g, a->k_stride_row, a->k_stride_bh, "k", 128,
+                     f16)))
+    return rc;
+  if ((rc = make_map(&tv, a->v, a->h, a->nk, a->bh / g, a->v_stride_row, a->v_stride_bh, "v", 128,
+                     f16)))
+    return rc;
   if ((rc = make_map(&tdo, a->dout, a->h, a->nq, a->bh, a->do_stride_row, a->do_stride_bh, "dout",
-                     qt)))
+                     qt, f16)))
     return rc;
   return launch_tile_bwd(*a, tq, tk, tv, tdo, static_cast<cudaStream_t>(stream));
 }
@@ -264,7 +291,7 @@ int a2d_bwd_finalize(const float* dq_acc, int64_t acc_stride_bh, int64_t acc_str
   if (!dq_acc || !dq) return set_error(A2D_EINVAL, "null pointer");
   if (h % 4 || acc_stride_bh % 4 || acc_stride_row % 4 || dq_stride_bh % 4 || dq_stride_row % 4)
     return set_error(A2D_EINVAL, "h and strides must be multiples of 4");
-  if (out_dtype != A2D_F32 && out_dtype != A2D_BF16) return set_error(A2D_EINVAL, "out_dtype invalid");
+  if (!out16_ok(out_dtype)) return set_error(A2D_EINVAL, "out_dtype invalid");
   return launch_bwd_finalize(dq_acc, acc_stride_bh, acc_stride_row, dq, out_dtype, dq_stride_bh,
                              dq_stride_row, bh, n, h, scale, static_cast<cudaStream_t>(stream));
 }
@@ -279,7 +306,7 @@ int a2d_lse_merge(const float* o_parts, const float* lse_parts, int32_t k_parts,
   if (rows < 0) return set_error(A2D_EINVAL, "negative sizes");
   if (rows == 0) return A2D_OK;
   if (!o_parts || !lse_parts || !o_out || !lse_out) return set_error(A2D_EINVAL, "null pointer");
-  if (out_dtype != A2D_F32 && out_dtype != A2D_BF16) return set_error(A2D_EINVAL, "out_dtype invalid");
+  if (!out16_ok(out_dtype)) return set_error(A2D_EINVAL, "out_dtype invalid");
   return launch_lse_merge(o_parts, lse_parts, k_parts, part_stride_o, part_stride_lse, rows, h,
                           row_stride, o_out, out_dtype, out_row_stride, lse_out,
                           static_cast<cudaStream_t>(stream));

@@ -21,7 +21,7 @@ int launch_lse_merge(const float* o_parts, const float* lse_parts, int k_parts,
                      float* lse_out, cudaStream_t stream);
 int launch_bwd_preprocess(const void* o, const void* dout, float* delta, long long o_sbh,
                           long long o_srow, long long do_sbh, long long do_srow, int bh, int n,
-                          int h, cudaStream_t stream);
+                          int h, bool f16, cudaStream_t stream);
 int launch_bwd_finalize(const float* dq_acc, long long asbh, long long asrow, void* dq,
                         int out_dtype, long long sbh, long long srow, int bh, int n, int h,
                         float scale, cudaStream_t stream);

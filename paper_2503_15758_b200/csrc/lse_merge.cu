@@ -9,12 +9,28 @@
 //   * dq = scale * dq_acc: the backward's final scaling (numpy_backend.py:61).
 // One warp per row, 16-byte vector loads, streaming cache hints.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include "kernels.h"
 
 namespace a2d {
 namespace {
 
 constexpr int kMaxParts = 16;
+
+// four fp32 -> four 16-bit outputs (A2D_BF16 or A2D_F16), round to nearest
+__device__ __forceinline__ uint2 pack4(int dtype, float4 v) {
+  uint2 u;
+  if (dtype == A2D_F16) {
+    __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+  } else {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+  }
+  return u;
+}
 
 __device__ __forceinline__ float4 ld_stream_f4(const float* p) {
   float4 v;
@@ -79,20 +95,23 @@ __global__ void __launch_bounds__(256) lse_merge_kernel(
       if (out_dtype == A2D_F32) {
         __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(o_out) + row * out_rs + e), acc);
       } else {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y);
-        __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z, acc.w);
-        uint2 u;
-        u.x = *reinterpret_cast<uint32_t*>(&lo);
-        u.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o_out) + row * out_rs + e) = u;
+        *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(o_out) + row * out_rs + e) =
+            pack4(out_dtype, acc);
       }
       if (lane == 0 && e == 0) lse_out[row] = tot > 0.f ? mx + __logf(tot) : -INFINITY;
     }
   }
 }
 
+template <bool F16>
+__device__ __forceinline__ float2 to_f2(uint32_t u) {
+  if (F16) return __half22float2(*reinterpret_cast<const __half2*>(&u));
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+}
+
+template <bool F16>
 __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
-    const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+    const uint16_t* __restrict__ o, const uint16_t* __restrict__ dout,
     float* __restrict__ delta, long long o_sbh, long long o_srow, long long do_sbh,
     long long do_srow, int bh, int n, int h) {
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -100,16 +119,14 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
   if (gw >= (long long)bh * n) return;
   const int b = (int)(gw / n);
   const int r = (int)(gw - (long long)b * n);
-  const __nv_bfloat16* po = o + b * o_sbh + (long long)r * o_srow;
-  const __nv_bfloat16* pd = dout + b * do_sbh + (long long)r * do_srow;
+  const uint16_t* po = o + b * o_sbh + (long long)r * o_srow;
+  const uint16_t* pd = dout + b * do_sbh + (long long)r * do_srow;
   float acc = 0.f;
   for (int e = lane * 4; e < h; e += 128) {
     const uint2 uo = *reinterpret_cast<const uint2*>(po + e);
     const uint2 ud = *reinterpret_cast<const uint2*>(pd + e);
-    const float2 o0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uo.x));
-    const float2 o1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uo.y));
-    const float2 d0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ud.x));
-    const float2 d1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ud.y));
+    const float2 o0 = to_f2<F16>(uo.x), o1 = to_f2<F16>(uo.y);
+    const float2 d0 = to_f2<F16>(ud.x), d1 = to_f2<F16>(ud.y);
     acc += o0.x * d0.x + o0.y * d0.y + o1.x * d1.x + o1.y * d1.y;
   }
 #pragma unroll
@@ -139,12 +156,7 @@ __global__ void __launch_bounds__(256) bwd_finalize_kernel(const float* __restri
     if (out_dtype == A2D_F32) {
       *reinterpret_cast<float4*>(reinterpret_cast<float*>(dq) + dst) = v;
     } else {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
-      __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
-      uint2 u;
-      u.x = *reinterpret_cast<uint32_t*>(&lo);
-      u.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(dq) + dst) = u;
+      *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(dq) + dst) = pack4(out_dtype, v);
     }
   }
 }
@@ -176,13 +188,15 @@ int launch_lse_merge(const float* o_parts, const float* lse_parts, int k_parts,
 
 int launch_bwd_preprocess(const void* o, const void* dout, float* delta, long long o_sbh,
                           long long o_srow, long long do_sbh, long long do_srow, int bh, int n,
-                          int h, cudaStream_t stream) {
+                          int h, bool f16, cudaStream_t stream) {
   const long long rows = (long long)bh * n;
   if (rows == 0) return A2D_OK;
   const int warps = 8;
-  bwd_preprocess_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout),
-      delta, o_sbh, o_srow, do_sbh, do_srow, bh, n, h);
+  const unsigned blocks = (unsigned)((rows + warps - 1) / warps);
+  auto kern = f16 ? bwd_preprocess_kernel<true> : bwd_preprocess_kernel<false>;
+  kern<<<blocks, warps * 32, 0, stream>>>(reinterpret_cast<const uint16_t*>(o),
+                                          reinterpret_cast<const uint16_t*>(dout), delta, o_sbh,
+                                          o_srow, do_sbh, do_srow, bh, n, h);
   return check_launch("bwd_preprocess_kernel");
 }
 

@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include "../../include/attn2d_b200.h"
 
 #define A2D_DEV __device__ __forceinline__
 
@@ -252,13 +253,13 @@ A2D_DEV void umma_commit(uint32_t bar) {
                : "memory");
 }
 
-// Instruction descriptor, kind::f16: bf16 A/B, fp32 D.
-//   [4,6) c_format=1 (F32)  [7,10) a_format=1 (BF16)  [10,13) b_format=1 (BF16)
+// Instruction descriptor, kind::f16: bf16 (or fp16) A/B, fp32 D.
+//   [4,6) c_format=1 (F32)  [7,10) a_format  [10,13) b_format (1 = BF16, 0 = F16)
 //   [15] a_major  [16] b_major (0 = K-major, 1 = MN-major)
 //   [17,23) N>>3  [24,29) M>>4
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, int a_mn_major,
-                                                       int b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn_major) << 15) |
+                                                       int b_mn_major, bool f16 = false) {
+  return (1u << 4) | (f16 ? 0u : (1u << 7) | (1u << 10)) | (uint32_t(a_mn_major) << 15) |
          (uint32_t(b_mn_major) << 16) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
@@ -370,6 +371,31 @@ A2D_DEV uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
+}
+A2D_DEV uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// the 16-bit operand type of the MMAs: bf16 (default) or fp16
+template <bool F16>
+A2D_DEV uint32_t pack2(float lo, float hi) {
+  return F16 ? pack_f16(lo, hi) : pack_bf16(lo, hi);
+}
+template <bool F16>
+A2D_DEV float2 unpack2(uint32_t p) {
+  if (F16) {
+    float2 f;
+    asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+        "cvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+        : "=f"(f.x), "=f"(f.y) : "r"(p));
+    return f;
+  }
+  return make_float2(__uint_as_float(p << 16), __uint_as_float(p & 0xffff0000u));
+}
+// 16-bit output element of an epilogue (A2D_BF16 or A2D_F16)
+A2D_DEV uint32_t pack_out(int dtype, float lo, float hi) {
+  return dtype == A2D_F16 ? pack_f16(lo, hi) : pack_bf16(lo, hi);
 }
 A2D_DEV void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),

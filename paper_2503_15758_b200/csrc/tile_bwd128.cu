@@ -76,6 +76,8 @@ constexpr int SMEM = OFF_TMEMPTR + 16;
 static_assert(SMEM <= 232448, "shared memory budget");
 constexpr uint32_t TM_DV = 0, TM_DK = 128, TM_X = 256, TM_Y = 384;
 
+// F16: fp16 Q/K/V/dO, P and dS (bf16 otherwise)
+template <bool F16>
 __global__ void __launch_bounds__(THREADS, 1)
     bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
@@ -138,9 +140,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   // h < 128: ceil(h/16) K steps for K Q^T / V dO^T and N = 16 ceil(h/16)
   // for dV / dK (the tiles' other head columns are zero fill)
   const int ksteps = (p.h + 15) / 16;
-  constexpr uint32_t id_ss = make_idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
-  const uint32_t id_kmn = make_idesc_bf16(128, ksteps * 16, 0, 1);  // P^T dO, dS^T Q
-  constexpr uint32_t id_mnmn = make_idesc_bf16(128, 128, 1, 1); // K^T dS^T
+  constexpr uint32_t id_ss = make_idesc_bf16(128, 128, 0, 0, F16);   // K Q^T, V dO^T
+  const uint32_t id_kmn = make_idesc_bf16(128, ksteps * 16, 0, 1, F16);  // P^T dO, dS^T Q
+  constexpr uint32_t id_mnmn = make_idesc_bf16(128, 128, 1, 1, F16); // K^T dS^T
   // K-major SW128: +32 B per K16 step inside a slab, +SLAB per 64 columns;
   // MN-major SW128: +2048 B per K16 step (16 rows of 128 B)
   auto kofs = [](int kk) { return uint64_t(((kk >> 2) * SLAB + (kk & 3) * 32) >> 4); };
@@ -377,7 +379,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const float2 x = ffma2(make_float2(pr[c], pr[c + 1]), sc,
                                  make_float2(-s_lse[c], -s_lse[c + 1]));
           const float2 e = B_POLY(c) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          pk[c >> 1] = pack_bf16(e.x, e.y);
+          pk[c >> 1] = pack2<F16>(e.x, e.y);
         }
       } else {
 #pragma unroll
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                  make_float2(-s_lse[c], -s_lse[c + 1]));
           const float e0 = (c0 + c >= first) ? ex2(x.x) : 0.f;
           const float e1 = (c0 + c + 1 >= first) ? ex2(x.y) : 0.f;
-          pk[c >> 1] = pack_bf16(e0, e1);
+          pk[c >> 1] = pack2<F16>(e0, e1);
         }
       }
       // P^T (bf16 pairs) over the first 32 columns of this warpgroup's S slice
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
       mbar_wait(bar(B_DPFULL), i & 1);
       tc_fence_after();
-      // dS = P (dP - delta), with P re-read from its bf16 pairs (the same
+      // dS = P (dP - delta), with P re-read from its 16-bit pairs (the same
       // rounded P that fed dV)
       float dpa[64];
       tmem_ld32(tmem + lane_addr + TM_Y + c0, dpa);
@@ -410,9 +412,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < 32; c += 2) {
           const float2 d = fadd2(make_float2(dp[c], dp[c + 1]),
                                  make_float2(-s_del[32 * h + c], -s_del[32 * h + c + 1]));
-          const uint32_t pp = pk[(32 * h + c) >> 1];
-          const float2 pf = make_float2(__uint_as_float(pp << 16), __uint_as_float(pp & 0xffff0000u));
-          pk[(32 * h + c) >> 1] = pack_bf16(pf.x * d.x, pf.y * d.y);
+          const float2 pf = unpack2<F16>(pk[(32 * h + c) >> 1]);
+          pk[(32 * h + c) >> 1] = pack2<F16>(pf.x * d.x, pf.y * d.y);
         }
       }
       // dS^T (bf16 pairs) into this warpgroup's first 32 columns of Y: the
@@ -463,16 +464,16 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           *reinterpret_cast<float4*>(dst + e) = w;
         }
-      } else {
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(base) + off;
+      } else {  // bf16 or fp16 dK / dV
+        uint16_t* dst = reinterpret_cast<uint16_t*>(base) + off;
 #pragma unroll
         for (int e = 0; e < 32; e += 8) {
           if (c * 32 + e >= p.h) continue;
           uint4 u;
-          u.x = pack_bf16(v[e] * mul, v[e + 1] * mul);
-          u.y = pack_bf16(v[e + 2] * mul, v[e + 3] * mul);
-          u.z = pack_bf16(v[e + 4] * mul, v[e + 5] * mul);
-          u.w = pack_bf16(v[e + 6] * mul, v[e + 7] * mul);
+          u.x = pack_out(p.dkv_dtype, v[e] * mul, v[e + 1] * mul);
+          u.y = pack_out(p.dkv_dtype, v[e + 2] * mul, v[e + 3] * mul);
+          u.z = pack_out(p.dkv_dtype, v[e + 4] * mul, v[e + 5] * mul);
+          u.w = pack_out(p.dkv_dtype, v[e + 6] * mul, v[e + 7] * mul);
           *reinterpret_cast<uint4*>(dst + e) = u;
         }
       }
@@ -535,14 +536,15 @@ int bwd_q_tile_rows(int) { return TILE; }
 
 int launch_tile_bwd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                   const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream) {
-  static bool configured[64] = {false};
+  static bool configured[2][64] = {};
+  const bool f16 = a.in_dtype == A2D_F16;
+  auto kern = f16 ? bwd128_kernel<true> : bwd128_kernel<false>;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!configured[dev & 63]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(bwd128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  if (!configured[f16][dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(bwd128)");
-    configured[dev & 63] = true;
+    configured[f16][dev & 63] = true;
   }
   CUtensorMap tdq;
   int rc = make_map_f32_dq_flat(&tdq, a.dq_acc, a.h, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh,
@@ -552,7 +554,7 @@ int launch_tile_bwd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUt
                           ? a.k_map.nblocks * (a.k_map.rows_per_block / TILE)
                           : (a.nk + TILE - 1) / TILE;
   dim3 grid(k_tiles, a.bh);
-  bwd128_kernel<<<grid, THREADS, SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+  kern<<<grid, THREADS, SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
   return check_launch("bwd128_kernel");
 }
 

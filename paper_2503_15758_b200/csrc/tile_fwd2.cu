@@ -144,17 +144,17 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
             *reinterpret_cast<float4*>(dst + i) =
                 make_float4(o[i] * w_new, o[i + 1] * w_new, o[i + 2] * w_new, o[i + 3] * w_new);
       }
-    } else {
-      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.o) + (long long)bh * p.o_stride_bh +
-                           (long long)grow * p.o_stride_row + col0 + c * 32;
+    } else {  // final O in bf16 or fp16
+      uint16_t* dst = reinterpret_cast<uint16_t*>(p.o) + (long long)bh * p.o_stride_bh +
+                      (long long)grow * p.o_stride_row + col0 + c * 32;
 #pragma unroll
       for (int i = 0; i < 32; i += 8) {
         if (col0 + c * 32 + i >= p.h) continue;
         uint4 v;
-        v.x = pack_bf16(o[i + 0] * w_new, o[i + 1] * w_new);
-        v.y = pack_bf16(o[i + 2] * w_new, o[i + 3] * w_new);
-        v.z = pack_bf16(o[i + 4] * w_new, o[i + 5] * w_new);
-        v.w = pack_bf16(o[i + 6] * w_new, o[i + 7] * w_new);
+        v.x = pack_out(p.o_dtype, o[i + 0] * w_new, o[i + 1] * w_new);
+        v.y = pack_out(p.o_dtype, o[i + 2] * w_new, o[i + 3] * w_new);
+        v.z = pack_out(p.o_dtype, o[i + 4] * w_new, o[i + 5] * w_new);
+        v.w = pack_out(p.o_dtype, o[i + 6] * w_new, o[i + 7] * w_new);
         *reinterpret_cast<uint4*>(dst + i) = v;
       }
     }
@@ -163,7 +163,8 @@ __device__ __forceinline__ void f2_epilogue(const a2d_tile_fwd_args& p, uint32_t
 
 constexpr int F2_THREADS = 384;  // producer/MMA warpgroup + 8 softmax warps
 
-template <int HD>
+// F16: fp16 Q/K/V and P (bf16 otherwise); everything else is shared
+template <int HD, bool F16>
 __global__ void __launch_bounds__(F2_THREADS, 1)
     fwd2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ a2d_tile_fwd_args p,
@@ -260,8 +261,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       // head dims below the tile width: only ceil(h/16) K steps for Q K^T and
       // an N = 16 ceil(h/16) PV (the tile's other columns are zero fill)
       const int ksteps = (p.h + 15) / 16;
-      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
-      const uint32_t idesc_pv = make_idesc_bf16(128, ksteps * 16, 0, 1);
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0, F16);
+      const uint32_t idesc_pv = make_idesc_bf16(128, ksteps * 16, 0, 1, F16);
       int ks = 0, kph = 0, vs = 0, vph = 0;
       mbar_wait_sleep(bar(L::B_Q), 0);
       // Descriptors are built once; per MMA only a constant is added to the
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
             const float2 x = ffma2(make_float2(s[jj], s[jj + 1]), sc, nb);
             const float2 e = make_float2(ex2(x.x), ex2(x.y));
             acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
-            pk[jj / 2] = pack_bf16(e.x, e.y);
+            pk[jj / 2] = pack2<F16>(e.x, e.y);
           }
         } else {  // some exponentials on the FMA pipe (MUFU offload, F2_POLY)
 #pragma unroll
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
             if (F2_POLY(jj)) e = exp2_poly2(x);
             else e = make_float2(ex2(x.x), ex2(x.y));
             acc[(jj >> 1) & 3] = fadd2(acc[(jj >> 1) & 3], e);
-            pk[jj / 2] = pack_bf16(e.x, e.y);
+            pk[jj / 2] = pack2<F16>(e.x, e.y);
           }
         }
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
@@ -448,7 +449,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       // row's first visible tile.  Values above 1 are exact in bf16 / fp32
       // (relative precision), so the max only has to move when a tile's sum
       // nears overflow (>= 2^64, or non-finite) — then it is recomputed
-      // exactly and the tile redone.
+      // exactly and the tile redone.  fp16 P has a 2^16 range, so there the
+      // bound is a tile sum of 2^15 (every element then fits).
       if (__any_sync(0xffffffffu, m_run == -INFINITY)) {
         const float m_new = fmaxf(m_run, rowmax<NC>(s) * sl2);
         if (m_new > m_run) {
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       }
       TR(2 * 8 + t * 4 + quarter, j);
       float tsum = exps(m_run == -INFINITY ? 0.f : m_run);
-      if (__any_sync(0xffffffffu, !(tsum < 0x1p64f))) {  // rare: S is still in TMEM
+      if (__any_sync(0xffffffffu, !(tsum < (F16 ? 0x1p15f : 0x1p64f)))) {  // rare: S still in TMEM
         load_s();
         const float m_new = fmaxf(m_run, rowmax<NC>(s) * sl2);
         if (m_new > m_run) {
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
 
 }  // namespace
 
-template <int HD>
+template <int HD, bool F16>
 int launch_fwd2_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                    const CUtensorMap& tv, cudaStream_t stream) {
   using L = F2Layout<HD>;
@@ -522,7 +524,7 @@ int launch_fwd2_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUte
   int dev = 0;
   cudaGetDevice(&dev);
   if (!configured[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(fwd2_kernel<HD>,
+    cudaError_t e = cudaFuncSetAttribute(fwd2_kernel<HD, F16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fwd2)");
     configured[dev & 63] = true;
@@ -531,15 +533,19 @@ int launch_fwd2_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUte
                           ? a.q_map.nblocks * (a.q_map.rows_per_block / TILE)
                           : (a.nq + TILE - 1) / TILE;
   dim3 grid((q_tiles + 1) / 2, a.bh);
-  fwd2_kernel<HD><<<grid, F2_THREADS, L::SMEM, stream>>>(tq, tk, tv, a, q_tiles);
+  fwd2_kernel<HD, F16><<<grid, F2_THREADS, L::SMEM, stream>>>(tq, tk, tv, a, q_tiles);
   return check_launch("fwd2_kernel");
 }
 
 int launch_tile_fwd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, cudaStream_t stream) {
   // tiles are 64 or 128 columns wide; columns past h are TMA zero fill
-  if (a.h > 64) return launch_fwd2_hd<128>(a, tq, tk, tv, stream);
-  return launch_fwd2_hd<64>(a, tq, tk, tv, stream);
+  const bool f16 = a.in_dtype == A2D_F16;
+  if (a.h > 64)
+    return f16 ? launch_fwd2_hd<128, true>(a, tq, tk, tv, stream)
+               : launch_fwd2_hd<128, false>(a, tq, tk, tv, stream);
+  return f16 ? launch_fwd2_hd<64, true>(a, tq, tk, tv, stream)
+             : launch_fwd2_hd<64, false>(a, tq, tk, tv, stream);
 }
 
 }  // namespace a2d

@@ -1,5 +1,5 @@
 """Single-device exact attention as a torch.autograd.Function — the 1x1 grid
-of Attention2D: one tile forward (finalize fused, bf16 O + fp32 LSE saved)
+of Attention2D: one tile forward (finalize fused, 16-bit O + fp32 LSE saved)
 and one tile backward.  The saved state is (Q, K, V, O, LSE), the LSE form of
 the reference's SavedState (strategies/common.py:64-80; PAPER Alg. 1
 SaveForBackprop)."""
@@ -15,7 +15,7 @@ from .errors import ShapeError
 class _TileAttention(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, causal: bool, scale: float):
-        o, lse = ops.tile_forward(q, k, v, causal=causal, scale=scale, out_dtype=torch.bfloat16)
+        o, lse = ops.tile_forward(q, k, v, causal=causal, scale=scale, out_dtype=q.dtype)
         ctx.save_for_backward(q, k, v, o, lse)
         ctx.causal, ctx.scale = causal, scale
         return o
@@ -23,7 +23,7 @@ class _TileAttention(torch.autograd.Function):
     @staticmethod
     def backward(ctx, do):
         q, k, v, o, lse = ctx.saved_tensors
-        do = do.to(torch.bfloat16)
+        do = do.to(q.dtype)
         if do.stride(-1) != 1:
             do = do.contiguous()
         dq, dk, dv = attention_backward(q, k, v, o, lse, do, ctx.causal, ctx.scale)
@@ -32,7 +32,7 @@ class _TileAttention(torch.autograd.Function):
 
 def attention_backward(q, k, v, o, lse, do, causal: bool, scale: float,
                        dq_acc: torch.Tensor | None = None):
-    """(dq, dk, dv) in bf16 for [bh, n, h] operands (k/v may have bh / g
+    """(dq, dk, dv) in q's dtype (bf16 or fp16) for [bh, n, h] operands (k/v may have bh / g
     heads: GQA / MQA, their gradients summed over each group of g query
     heads in fp32)."""
     delta = ops.bwd_preprocess(o, do)
@@ -43,18 +43,18 @@ def attention_backward(q, k, v, o, lse, do, causal: bool, scale: float,
     group = q.shape[0] // k.shape[0]
     dq_acc, dk, dv = ops.tile_backward(q, k, v, do, lse, delta, causal=causal, scale=scale,
                                        dq_acc=dq_acc,
-                                       dkv_dtype=torch.bfloat16 if group == 1 else torch.float32)
+                                       dkv_dtype=q.dtype if group == 1 else torch.float32)
     if group > 1:
-        dk, dv = (t.view(k.shape[0], group, *t.shape[1:]).sum(1).to(torch.bfloat16)
-                  for t in (dk, dv))
-    dq = ops.bwd_finalize(dq_acc, scale, dtype=torch.bfloat16)
+        dk, dv = (t.view(k.shape[0], group, *t.shape[1:]).sum(1).to(q.dtype) for t in (dk, dv))
+    dq = ops.bwd_finalize(dq_acc, scale, dtype=q.dtype)
     return dq, dk, dv
 
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = False,
               scale: float | None = None) -> torch.Tensor:
     """softmax(scale q k^T [+ causal]) v for q of shape [B, M, N, H] or
-    [BH, N, H], bf16, on one B200.  k/v have the same shape, or M_kv heads
+    [BH, N, H], bf16 or fp16, on one B200 (output and gradients in the
+    input dtype).  k/v have the same shape, or M_kv heads
     with M_kv dividing M (grouped-query / multi-query attention: query head
     m reads k/v head m // (M / M_kv)).  scale defaults to 1/sqrt(H)."""
     if q.dim() not in (3, 4) or k.shape != v.shape or k.dim() != q.dim():

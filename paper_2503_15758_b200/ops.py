@@ -148,13 +148,21 @@ def _stream(t: torch.Tensor) -> int:
     return torch.cuda.current_stream(t.device).cuda_stream
 
 
-def _check3(name: str, t: torch.Tensor, dtype=torch.bfloat16):
+# 16-bit operand types of the tile kernels (tcgen05 kind::f16)
+INPUT_DTYPES = (torch.bfloat16, torch.float16)
+
+
+def _check3(name: str, t: torch.Tensor, dtype=None):
+    """[bh, rows, h] CUDA tensor with unit stride along h, of `dtype` (or,
+    when None, of one of the 16-bit input types)."""
     if not t.is_cuda:
         raise ShapeError(f"{name} must be a CUDA tensor")
     if t.dim() != 3:
         raise ShapeError(f"{name} must be [bh, rows, h], got {tuple(t.shape)}")
-    if t.dtype != dtype:
-        raise ShapeError(f"{name} must be {dtype}, got {t.dtype}")
+    if dtype is None and t.dtype not in INPUT_DTYPES:
+        raise ShapeError(f"{name} must be torch.bfloat16 or torch.float16, got {t.dtype}")
+    if dtype is not None and t.dtype != dtype:
+        raise ShapeError(f"{name} must be {dtype} like the other operands, got {t.dtype}")
     if t.shape[2] > 0 and t.stride(2) != 1:
         raise ShapeError(f"{name} must have unit stride along h")
 
@@ -164,6 +172,8 @@ def _dtype_code(dt: torch.dtype) -> int:
         return _lib.F32
     if dt == torch.bfloat16:
         return _lib.BF16
+    if dt == torch.float16:
+        return _lib.F16
     raise UnsupportedError(f"output dtype {dt} not supported")
 
 
@@ -179,14 +189,16 @@ def tile_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: b
     """Partial attention of q against exactly the keys in k/v.  k/v may hold
     fewer heads than q (GQA / MQA): query head b reads k/v head b // group.
 
-    Returns (o, lse): o [bh, nq, h] (fp32 normalised partial, or bf16 final),
+    q/k/v are bf16 or fp16 (all alike).
+    Returns (o, lse): o [bh, nq, h] (fp32 normalised partial, or final O in
+    bf16 / fp16),
     lse [bh, nq] fp32, -inf where a row attended nothing.  With accumulate,
     (out, lse) hold a previous partial and are merged in place.
     """
     lib = _lib.load()
     _check3("q", q)
-    _check3("k", k)
-    _check3("v", v)
+    _check3("k", k, q.dtype)
+    _check3("v", v, q.dtype)
     bh, nq, h = q.shape
     nk = k.shape[1]
     group = _kv_group(bh, k)
@@ -225,6 +237,7 @@ def tile_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: b
     a.accumulate = int(bool(accumulate))
     a.q_map, a.k_map = qi.to_c(), ki.to_c()
     a.kv_group = group
+    a.in_dtype = _dtype_code(q.dtype)
     _lib.check(lib.a2d_tile_fwd(a, _stream(q)), "a2d_tile_fwd")
     return out, lse
 
@@ -233,14 +246,15 @@ def bwd_preprocess(o: torch.Tensor, dout: torch.Tensor) -> torch.Tensor:
     """delta = rowsum(dO * O) in fp32 (numpy_backend.py:49)."""
     lib = _lib.load()
     _check3("o", o)
-    _check3("dout", dout)
+    _check3("dout", dout, o.dtype)
     if o.shape != dout.shape:
         raise ShapeError("o and dout differ in shape")
     bh, n, h = o.shape
     delta = torch.empty((bh, n), dtype=torch.float32, device=o.device)
     _lib.check(lib.a2d_bwd_preprocess(o.data_ptr(), dout.data_ptr(), delta.data_ptr(),
                                       o.stride(0), o.stride(1), dout.stride(0), dout.stride(1),
-                                      bh, n, h, _stream(o)), "a2d_bwd_preprocess")
+                                      bh, n, h, _dtype_code(o.dtype), _stream(o)),
+               "a2d_bwd_preprocess")
     return delta
 
 
@@ -258,8 +272,9 @@ def tile_backward(q, k, v, dout, lse, delta, *, causal: bool, scale: float,
     Returns (dq_acc, dk, dv).
     """
     lib = _lib.load()
-    for name, t in (("q", q), ("k", k), ("v", v), ("dout", dout)):
-        _check3(name, t)
+    _check3("q", q)
+    for name, t in (("k", k), ("v", v), ("dout", dout)):
+        _check3(name, t, q.dtype)
     bh, nq, h = q.shape
     nk = k.shape[1]
     group = _kv_group(bh, k)
@@ -303,6 +318,7 @@ def tile_backward(q, k, v, dout, lse, delta, *, causal: bool, scale: float,
     a.accumulate_dkv = int(bool(accumulate_dkv))
     a.q_map, a.k_map = qi.to_c(), ki.to_c()
     a.kv_group = group
+    a.in_dtype = _dtype_code(q.dtype)
     _lib.check(lib.a2d_tile_bwd(a, _stream(q)), "a2d_tile_bwd")
     return dq_acc, dk, dv
 

@@ -79,11 +79,11 @@ class Attention2D:
         g, L = self.grid, self.L
         bh, h = q_g.shape[1], q_g.shape[2]
         if g.pc == 1:
-            o = torch.empty((L, bh, h), dtype=torch.bfloat16, device=q_g.device)
+            o = torch.empty((L, bh, h), dtype=q_g.dtype, device=q_g.device)
             lse = torch.empty((bh, L), dtype=torch.float32, device=q_g.device)
             self.ops.tile_forward(_heads(q_g), _heads(k_g), _heads(v_g), causal=self.causal,
                                   scale=self.scale, q_index=self.q_index, k_index=self.k_index,
-                                  out=_heads(o), lse=lse, out_dtype=torch.bfloat16)
+                                  out=_heads(o), lse=lse, out_dtype=q_g.dtype)
             return o, lse.t().contiguous()
         o_part = torch.empty((g.pc * L, bh, h), dtype=torch.float32, device=q_g.device)
         lse_part = torch.empty((bh, g.pc * L), dtype=torch.float32, device=q_g.device)
@@ -92,11 +92,11 @@ class Attention2D:
                               out=_heads(o_part), lse=lse_part)
         return o_part, lse_part.t().contiguous()
 
-    def _merge(self, recv_o, recv_lse):
+    def _merge(self, recv_o, recv_lse, dtype):
         g, L = self.grid, self.L
         bh, h = recv_o.shape[1], recv_o.shape[2]
         o, lse = self.ops.lse_merge(recv_o.view(g.pc, L * bh, h), recv_lse.view(g.pc, L * bh),
-                                    out_dtype=torch.bfloat16)
+                                    out_dtype=dtype)
         return o.view(L, bh, h), lse.view(L, bh)
 
     def forward(self, q_p: torch.Tensor, k_p: torch.Tensor, v_p: torch.Tensor):
@@ -130,12 +130,12 @@ class Attention2D:
             if pending is not None:
                 j, po, pl, pw = pending
                 wait_all(pw)
-                outs_o[j], outs_lse[j] = self._merge(po, pl)
+                outs_o[j], outs_lse[j] = self._merge(po, pl, q_p.dtype)
             pending = (i, ro, rl, (w1, w2))
         if pending is not None:
             j, po, pl, pw = pending
             wait_all(pw)
-            outs_o[j], outs_lse[j] = self._merge(po, pl)
+            outs_o[j], outs_lse[j] = self._merge(po, pl, q_p.dtype)
         o_p = outs_o[0] if len(chunks) == 1 else torch.cat(outs_o, dim=1)
         lse_p = outs_lse[0] if len(chunks) == 1 else torch.cat(outs_lse, dim=1)
         return o_p, Saved2D(q=q_p, k=k_t, v=v_t, o=o_p, lse=lse_p)
@@ -172,7 +172,7 @@ class Attention2D:
             lse_g = st_g[..., 0].t().contiguous()
             delta_g = st_g[..., 1].t().contiguous()
             dq_acc = torch.zeros((g.pc * L, bh, h), dtype=torch.float32, device=q_g.device)
-            kdt = torch.float32 if g.pr > 1 else torch.bfloat16
+            kdt = torch.float32 if g.pr > 1 else saved.q.dtype
             dk_g = torch.empty((g.pr * L, bh, h), dtype=kdt, device=q_g.device)
             dv_g = torch.empty((g.pr * L, bh, h), dtype=kdt, device=q_g.device)
             self.ops.tile_backward(_heads(q_g), _heads(k_g), _heads(v_g), _heads(do_g), lse_g,
@@ -191,9 +191,10 @@ class Attention2D:
         dk_t = dk_parts[0] if len(chunks) == 1 else torch.cat(dk_parts, dim=1)
         dv_t = dv_parts[0] if len(chunks) == 1 else torch.cat(dv_parts, dim=1)
         dk_p, dv_p = comm.unpermute_kv(dk_t, dv_t)
-        dq_p = torch.empty((L, bh_all, h), dtype=torch.bfloat16, device=do_p.device)
+        dt = saved.q.dtype
+        dq_p = torch.empty((L, bh_all, h), dtype=dt, device=do_p.device)
         self.ops.bwd_finalize(_heads(dq_acc), self.scale, out=_heads(dq_p))
-        return dq_p, dk_p.to(torch.bfloat16), dv_p.to(torch.bfloat16)
+        return dq_p, dk_p.to(dt), dv_p.to(dt)
 
 
 class _Attention2DFn(torch.autograd.Function):
@@ -206,7 +207,7 @@ class _Attention2DFn(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, do_p):
-        dq, dk, dv = ctx.plan.backward(ctx.saved, do_p.to(torch.bfloat16).contiguous())
+        dq, dk, dv = ctx.plan.backward(ctx.saved, do_p.to(ctx.saved.q.dtype).contiguous())
         return dq, dk, dv, None
 
 

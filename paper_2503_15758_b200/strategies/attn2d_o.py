@@ -113,10 +113,10 @@ class Attention2DO:
         if g.pc > 1:
             self._row_sweep_fwd(q_next, k_g, v_g, fin_o, fin_l)
             o_hm, lse_hm = self.ops.lse_merge(fin_o.view(2, bh * L, h), fin_l.view(2, bh * L),
-                                              out_dtype=torch.bfloat16)
+                                              out_dtype=q_p.dtype)
         else:
             o_hm, lse_hm = self.ops.lse_merge(fin_o[:1].view(1, bh * L, h),
-                                              fin_l[:1].view(1, bh * L), out_dtype=torch.bfloat16)
+                                              fin_l[:1].view(1, bh * L), out_dtype=q_p.dtype)
         o_p = o_hm.view(bh, L, h).transpose(0, 1).contiguous()
         lse_p = lse_hm.view(bh, L).t().contiguous()
         return o_p, Saved2D(q=q_p, k=k_t, v=v_t, o=o_p, lse=lse_p)
@@ -213,9 +213,10 @@ class Attention2DO:
         else:
             dk_t, dv_t = dk_g, dv_g
         dk_p, dv_p = comm.unpermute_kv(dk_t, dv_t)
-        dq_p = torch.empty((L, bh, h), dtype=torch.bfloat16, device=dev)
+        dt = saved.q.dtype
+        dq_p = torch.empty((L, bh, h), dtype=dt, device=dev)
         self.ops.bwd_finalize(_heads(dq_acc), self.scale, out=_heads(dq_p))
-        return dq_p, dk_p.to(torch.bfloat16), dv_p.to(torch.bfloat16)
+        return dq_p, dk_p.to(dt), dv_p.to(dt)
 
     def _bwd_tile(self, bundle, q_index, k, v, k_index, dq, dk, dv, accumulate=False):
         q_b, do_b, st_b = bundle

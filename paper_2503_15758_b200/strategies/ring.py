@@ -54,7 +54,7 @@ class RingAttention:
                 wait_all(work)
                 cur_k, cur_v = nk, nv
             src = (src - 1) % self.p
-        o_p = o.to(torch.bfloat16)
+        o_p = o.to(q_p.dtype)
         lse_p = lse.t().contiguous()
         return o_p, Saved2D(q=q_p, k=k_p, v=v_p, o=o_p, lse=lse_p)
 
@@ -104,6 +104,7 @@ class RingAttention:
         if acc_work is not None:
             wait_all(acc_work[1])
             dk_acc, dv_acc = acc_work[0]
-        dq_p = torch.empty((rows, bh, h), dtype=torch.bfloat16, device=do_p.device)
+        dt = saved.q.dtype
+        dq_p = torch.empty((rows, bh, h), dtype=dt, device=do_p.device)
         self.ops.bwd_finalize(_heads(dq_acc), self.scale, out=_heads(dq_p))
-        return dq_p, dk_acc.to(torch.bfloat16), dv_acc.to(torch.bfloat16)
+        return dq_p, dk_acc.to(dt), dv_acc.to(dt)

@@ -176,8 +176,13 @@ def test_abi_empty_calls_succeed_with_null_buffers():
     assert lib.a2d_tile_fwd(a, None) == _lib.A2D_OK
     a.bh, a.nq, a.q_map.rows_per_block = 2, 0, 0
     assert lib.a2d_tile_fwd(a, None) == _lib.A2D_OK
-    assert lib.a2d_bwd_preprocess(None, None, None, 0, 0, 0, 0, 0, 128, 64, None) == _lib.A2D_OK
+    assert lib.a2d_bwd_preprocess(None, None, None, 0, 0, 0, 0, 0, 128, 64, _lib.BF16,
+                                  None) == _lib.A2D_OK
     assert lib.a2d_bwd_finalize(None, 0, 0, None, _lib.F32, 0, 0, 2, 0, 64, 1.0, None) == _lib.A2D_OK
     assert lib.a2d_lse_merge(None, None, 2, 0, 0, 0, 64, 64, None, _lib.F32, 64, None,
                              None) == _lib.A2D_OK
-    assert lib.a2d_bwd_preprocess(None, None, None, 0, 0, 0, 0, -1, 128, 64, None) == _lib.A2D_EINVAL
+    assert lib.a2d_bwd_preprocess(None, None, None, 0, 0, 0, 0, -1, 128, 64, _lib.F16,
+                                  None) == _lib.A2D_EINVAL
+    # 16-bit inputs only (0, the v3 reserved value, reads as bf16)
+    assert lib.a2d_bwd_preprocess(None, None, None, 0, 0, 0, 0, 1, 128, 64, 3,
+                                  None) == _lib.A2D_EUNSUPPORTED

@@ -1,5 +1,6 @@
 """Seeded random sweep of the tile kernels against a torch fp32 restatement:
-ragged row counts on both sides, head dims 8..128, GQA / MQA groups,
+ragged row counts on both sides, head dims 8..128, bf16 and fp16 operands,
+GQA / MQA groups,
 global-index maps (offset and strided affine maps, blocked cyclic maps,
 explicit index arrays, an array query map against an affine key map), causal and not, fp32 / bf16 outputs, rows with no
 visible key.  The backward is fed the reference's own (LSE, delta), so it
@@ -101,13 +102,14 @@ def test_random_tile_calls_match_torch(ops, case):
     bh = bh_kv * group
     causal = bool(rng.integers(0, 2))
     scale = float(rng.choice([h ** -0.5, 1.0]))
-    out_dtype = torch.float32 if rng.integers(0, 2) else torch.bfloat16
+    dt = torch.float16 if rng.integers(0, 3) == 0 else torch.bfloat16  # operand type
+    out_dtype = torch.float32 if rng.integers(0, 2) else dt
     tag = dict(kind=kind, nq=nq, nk=nk, h=h, group=group, bh=bh, causal=causal, scale=scale,
-               out=str(out_dtype))
+               dt=str(dt), out=str(out_dtype))
     g = torch.Generator(device="cpu").manual_seed(case)
 
     def rnd(*shape):
-        return (torch.rand(shape, generator=g) * 2 - 1).to(device="cuda", dtype=torch.bfloat16)
+        return (torch.rand(shape, generator=g) * 2 - 1).to(device="cuda", dtype=dt)
 
     q, dout = rnd(bh, nq, h), rnd(bh, nq, h)
     k, v = rnd(bh_kv, nk, h), rnd(bh_kv, nk, h)

@@ -359,12 +359,14 @@ def test_other_head_dims(ops, h):
         assert rel_fro(got, want) < REL_TOL
 
 
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("h", [64, 128])
 @pytest.mark.parametrize("causal", [False, True])
-def test_forward_growing_scores_move_the_running_max(ops, causal, h):
+def test_forward_growing_scores_move_the_running_max(ops, causal, h, dt):
     """Scores that grow by ~2^100 along the key sweep: the forward's running
     max (taken from the first visible tile, moved only when a tile's sum
-    nears overflow) must re-base exactly; compared with the fp32 reference."""
+    nears overflow: 2^64 with bf16 P, 2^15 with fp16 P) must re-base exactly;
+    compared with the fp32 reference."""
     bh, n = 2, 1024
     g = torch.Generator(device="cpu").manual_seed(7)
     u = torch.randn((h,), generator=g)
@@ -372,9 +374,9 @@ def test_forward_growing_scores_move_the_running_max(ops, causal, h):
     a = torch.linspace(0.5, 1.0, n)[:, None]                  # query rows
     b = torch.linspace(-10.0, 90.0, n)[:, None]               # key rows: growing scores
     noise = lambda: 0.05 * torch.randn((n, h), generator=g)   # noqa: E731
-    q = (a * u + noise()).expand(bh, n, h).contiguous().to("cuda", torch.bfloat16)
-    k = (b * u + noise()).expand(bh, n, h).contiguous().to("cuda", torch.bfloat16)
-    v = uniform((bh, n, h), 91)
+    q = (a * u + noise()).expand(bh, n, h).contiguous().to("cuda", dt)
+    k = (b * u + noise()).expand(bh, n, h).contiguous().to("cuda", dt)
+    v = uniform((bh, n, h), 91).to(dt)
     o, lse = ops.tile_forward(q, k, v, causal=causal, scale=1.0, out_dtype=torch.float32)
     want_o, want_lse = ref_attention(q, k, v, causal, 1.0)
     assert torch.isfinite(o).all() and torch.isfinite(lse).all()
@@ -431,9 +433,10 @@ def test_full_size_row_and_key_sampled_parity(ops, n, bh):
     assert rel_fro(vg.grad[:, keys], dv_ref) < REL_TOL
 
 
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("h", [64, 128])
 @pytest.mark.parametrize("col", [270, 271, 300, 330, 383])
-def test_forward_single_huge_score_on_any_column(ops, col, h):
+def test_forward_single_huge_score_on_any_column(ops, col, h, dt):
     """One key whose score exceeds every earlier tile's by ~2^200, placed on
     a column the forward evaluates with the FMA-pipe polynomial (270, 271)
     or with MUFU (300, 330, 383), in either key half of its tile: the
@@ -445,8 +448,8 @@ def test_forward_single_huge_score_on_any_column(ops, col, h):
     q = (u + 0.01 * torch.randn((n, h), generator=g))[None].contiguous()
     k = (0.01 * torch.randn((n, h), generator=g))[None].contiguous()
     k[0, col] = 140.0 * u
-    q, k = q.to("cuda", torch.bfloat16), k.to("cuda", torch.bfloat16)
-    v = uniform((bh, n, h), 93)
+    q, k = q.to("cuda", dt), k.to("cuda", dt)
+    v = uniform((bh, n, h), 93).to(dt)
     for causal in (False, True):
         o, lse = ops.tile_forward(q, k, v, causal=causal, scale=1.0, out_dtype=torch.float32)
         want_o, want_lse = ref_attention(q, k, v, causal, 1.0)
@@ -504,3 +507,44 @@ def test_forward_without_heads_or_rows_is_a_no_op(ops):
                                                               device="cuda")
         o, lse = ops.tile_forward(q, k, k, causal=True, scale=0.125)
         assert o.shape == (bh, nq, 64) and lse.shape == (bh, nq)
+
+
+@pytest.mark.parametrize("m,m_kv", [(4, 4), (4, 2)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_fp16_attention_fwd_bwd(ops, causal, m, m_kv):
+    """fp16 operands end to end (in_dtype A2D_F16: fp16 TMA maps, kind::f16
+    MMAs with fp16 A/B, fp16 P and dS): functional.attention forward and
+    backward in fp16 against the fp32 reference, GQA included."""
+    from paper_2503_15758_b200 import functional
+    from gpu_util import ref_attention_grad
+    n, h = 640, 128
+    scale = h ** -0.5
+    q, do = (uniform((m, n, h), 210 + i).to(torch.float16) for i in range(2))
+    k, v = (uniform((m_kv, n, h), 220 + i).to(torch.float16) for i in range(2))
+    qg, kg, vg = (x.clone().requires_grad_(True) for x in (q, k, v))
+    o = functional.attention(qg, kg, vg, causal=causal, scale=scale)
+    o.backward(do)
+    assert o.dtype == torch.float16 and qg.grad.dtype == torch.float16
+    rep = m // m_kv
+    kr, vr = k.repeat_interleave(rep, 0), v.repeat_interleave(rep, 0)
+    want_o, _ = ref_attention(q, kr, vr, causal, scale)
+    dq, dk, dv = ref_attention_grad(q, kr, vr, do, causal, scale)
+    dk = dk.view(m_kv, rep, n, h).sum(1)
+    dv = dv.view(m_kv, rep, n, h).sum(1)
+    assert rel_fro(o, want_o) < REL_TOL
+    for got, want in ((qg.grad, dq), (kg.grad, dk), (vg.grad, dv)):
+        assert rel_fro(got, want) < REL_TOL, rel_fro(got, want)
+
+
+def test_fp16_merge_and_finalize_outputs(ops):
+    """lse_merge and bwd_finalize write fp16 as they write bf16 (A2D_F16)."""
+    rows, h = 300, 128
+    o_parts = torch.randn((3, rows, h), device="cuda")
+    lse_parts = torch.randn((3, rows), device="cuda")
+    o16, lse16 = ops.lse_merge(o_parts, lse_parts, out_dtype=torch.float16)
+    o32, lse32 = ops.lse_merge(o_parts, lse_parts, out_dtype=torch.float32)
+    assert o16.dtype == torch.float16 and torch.equal(lse16, lse32)
+    assert max_abs(o16.float(), o32) <= float(o32.abs().max()) * 2 ** -10
+    acc = torch.randn((2, rows, h), device="cuda")
+    dq = ops.bwd_finalize(acc, 0.5, dtype=torch.float16)
+    assert torch.equal(dq, (acc * 0.5).to(torch.float16))
