@@ -72,7 +72,10 @@ enum {
   B_DPFULL, B_DSREADY, B_DSFREE, B_DQFULL, B_DQFREE, B_DONE, NBAR
 };
 constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
-constexpr int SMEM = OFF_TMEMPTR + 16;
+// the CTA's query-tile range, computed once by thread 0 and read by every
+// role from shared memory (a per-thread copy would live in local memory)
+constexpr int OFF_RANGE = OFF_TMEMPTR + 16;
+constexpr int SMEM = OFF_RANGE + (int(sizeof(TileRange)) + 15) / 16 * 16;
 static_assert(SMEM <= 232448, "shared memory budget");
 constexpr uint32_t TM_DV = 0, TM_DK = 128, TM_X = 256, TM_Y = 384;
 
@@ -94,7 +97,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   float* stat = reinterpret_cast<float*>(smem + OFF_STAT);
   if ((sb & 1023) != 0) __trap();
 
+  const bool causal = p.causal != 0;
+  const TileRef kt = tile_ref(p.k_map, p.nk, kt_idx * TILE);
   if (threadIdx.x == 0) {
+    query_range(p.q_map, p.nq, causal, kt.gmin, *reinterpret_cast<TileRange*>(smem + OFF_RANGE),
+                TILE);
     mbar_init(bar(B_KV), 1);
     mbar_init(bar(B_QFULL0), 2);  // TMA bytes + the producer's stats arrival
     mbar_init(bar(B_QFULL1), 2);
@@ -128,10 +135,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + OFF_TMEMPTR);
 
-  const bool causal = p.causal != 0;
-  const TileRef kt = tile_ref(p.k_map, p.nk, kt_idx * TILE);
-  TileRange qr;
-  query_range(p.q_map, p.nq, causal, kt.gmin, qr, TILE);
+  const TileRange& qr = *reinterpret_cast<const TileRange*>(smem + OFF_RANGE);
   const int n_tiles = qr.total;
   const int qrot = kt_idx;  // rotated q sweep: co-resident CTAs reduce into different dQ rows
 

@@ -79,7 +79,10 @@ struct F2Layout {
   static constexpr int B_ODONE = B_PFULL + 2;     // [2]: last PV_t done
   static constexpr int NBAR = B_ODONE + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBAR * 8;
-  static constexpr int SMEM = OFF_TMEMPTR + 16;
+  // the CTA's key-tile range, computed once by thread 0: every role reads it
+  // from shared memory (a per-thread copy would live in local memory)
+  static constexpr int OFF_RANGE = OFF_TMEMPTR + 16;
+  static constexpr int SMEM = OFF_RANGE + (int(sizeof(TileRange)) + 15) / 16 * 16;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -183,7 +186,15 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   auto bar = [&](int i) { return sb + L::OFF_BAR + 8 * i; };
   const uint32_t TM_O0 = 256, TM_O1 = 256 + HD;
 
+  const bool causal = p.causal != 0;
+  const int t0 = 2 * pair, t1 = 2 * pair + 1;
+  const bool has1 = t1 < q_tiles;
+  const TileRef qt0 = tile_ref(p.q_map, p.nq, t0 * TILE);
+  TileRef qt1 = qt0;
+  if (has1) qt1 = tile_ref(p.q_map, p.nq, t1 * TILE);
   if (threadIdx.x == 0) {
+    key_range(p.k_map, p.nk, causal, has1 ? max(qt0.gmax, qt1.gmax) : qt0.gmax,
+              *reinterpret_cast<TileRange*>(smem + L::OFF_RANGE));
     mbar_init(bar(L::B_Q), 1);
     for (int i = 0; i < L::KST; ++i) {
       mbar_init(bar(L::B_KFULL + i), 1);
@@ -214,19 +225,12 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + L::OFF_TMEMPTR);
 
-  const bool causal = p.causal != 0;
-  const int t0 = 2 * pair, t1 = 2 * pair + 1;
-  const bool has1 = t1 < q_tiles;
-  const TileRef qt0 = tile_ref(p.q_map, p.nq, t0 * TILE);
-  TileRef qt1 = qt0;
-  if (has1) qt1 = tile_ref(p.q_map, p.nq, t1 * TILE);
-  TileRange kr;
-  key_range(p.k_map, p.nk, causal, has1 ? max(qt0.gmax, qt1.gmax) : qt0.gmax, kr);
+  const TileRange& kr = *reinterpret_cast<const TileRange*>(smem + L::OFF_RANGE);
   const int n_tiles = kr.total;
   const int rot = pair;  // rotated key sweep
 
   if (warp < 4) {
-    regs_dec<96>();
+    regs_dec<80>();
     if (warp == 0 && lane == 0 && n_tiles > 0) {
       // -------------------------------------------------------- producer
       mbar_expect_tx(bar(L::B_Q), 2 * L::TILE_BYTES);
@@ -344,7 +348,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       }
     }
   } else {
-    regs_inc<200>();
+    regs_inc<208>();
     // ------------------------------------------------------------ softmax warps
     // warp w owns query tile t = (w-4)/4, all 128 key columns
     constexpr int NC = TILE;  // key columns of S per thread and tile

@@ -76,7 +76,23 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
     "fwdsleep": [(F, "#include \"kernels.h\"", "#include \"kernels.h\"\n#define mbar_wait mbar_wait_sleep")],
     "poly38": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)",
                 "#define B_POLY(c) ((((c) >> 1) & 7) == 1 || (((c) >> 1) & 7) == 4 || (((c) >> 1) & 7) == 6)")],
+    # forward: the two softmax warpgroups take turns in the exponential phase
+    # (named barriers 2/3, 256 threads): no MUFU sharing between the tiles
+    "fpp": [(F, "      float tsum = exps(m_run == -INFINITY ? 0.f : m_run);",
+             "      named_bar_sync(2 + t, 256);\n"
+             "      float tsum = exps(m_run == -INFINITY ? 0.f : m_run);\n"
+             "      named_bar_arrive(3 - t, 256);"),
+            (F, "    const TileRef qt = t ? qt1 : qt0;\n    for (int j = 0; j < n_tiles; ++j) {",
+             "    const TileRef qt = t ? qt1 : qt0;\n    if (t == 1 && n_tiles > 0) named_bar_arrive(2, 256);\n"
+             "    for (int j = 0; j < n_tiles; ++j) {"),
+            (F, "    // ------------------------------------------------------------ epilogue\n    if (n_tiles > 0) {",
+             "    // ------------------------------------------------------------ epilogue\n"
+             "    if (t == 0 && n_tiles > 0) named_bar_sync(2, 256);\n    if (n_tiles > 0) {")],
 }
+
+
+VARIANTS["fpp4"] = VARIANTS["fpp"] + VARIANTS["fpoly4"]
+VARIANTS["fpptrace"] = VARIANTS["fpp"] + VARIANTS["ftrace"]
 
 
 def build(name: str) -> Path:
