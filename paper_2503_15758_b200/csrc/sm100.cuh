@@ -315,6 +315,15 @@ A2D_DEV float2 fadd2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+A2D_DEV float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
 // 2^x for finite x <= ~8 on the FMA/ALU pipes (MUFU offload): round-to-nearest
 // split x = n + f, f in [-0.5, 0.5], near-minimax cubic for 2^f (max rel err
 // 1.0e-4, far below the bf16 rounding of P), 2^n folded into the exponent.

@@ -37,10 +37,6 @@
 #include "tiles.cuh"
 #include "kernels.h"
 
-// exponential pairs of the P phase evaluated on the FMA-pipe polynomial
-// (one in four; 0 and 1/8 measured equal)
-#define B_POLY(c) ((((c) >> 1) & 3) == 3)
-
 namespace a2d {
 namespace {
 
@@ -382,7 +378,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < 64; c += 2) {
           const float2 x = ffma2(make_float2(pr[c], pr[c + 1]), sc,
                                  make_float2(-s_lse[c], -s_lse[c + 1]));
-          const float2 e = B_POLY(c) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          // every exponential on MUFU: moving a quarter of them to the
+          // FMA-pipe polynomial measured 1-2% slower (profiles/r2_ab.md)
+          const float2 e = make_float2(ex2(x.x), ex2(x.y));
           pk[c >> 1] = pack2<F16>(e.x, e.y);
         }
       } else {
@@ -417,7 +415,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           const float2 d = fadd2(make_float2(dp[c], dp[c + 1]),
                                  make_float2(-s_del[32 * h + c], -s_del[32 * h + c + 1]));
           const float2 pf = unpack2<F16>(pk[(32 * h + c) >> 1]);
-          pk[(32 * h + c) >> 1] = pack2<F16>(pf.x * d.x, pf.y * d.y);
+          const float2 ds = fmul2(pf, d);
+          pk[(32 * h + c) >> 1] = pack2<F16>(ds.x, ds.y);
         }
       }
       // dS^T (bf16 pairs) into this warpgroup's first 32 columns of Y: the

@@ -91,6 +91,11 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
 }
 
 
+# backward dS = P (dP - delta) with one packed f32x2 multiply per pair
+VARIANTS["bfmul2"] = [(B, "pk[(32 * h + c) >> 1] = pack2<F16>(pf.x * d.x, pf.y * d.y);",
+                       "const float2 ds = fmul2(pf, d);\n          pk[(32 * h + c) >> 1] = pack2<F16>(ds.x, ds.y);")]
+VARIANTS["bpoly0"] = [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)", "#define B_POLY(c) false")]
+VARIANTS["bfmul2p0"] = VARIANTS["bfmul2"] + VARIANTS["bpoly0"]
 VARIANTS["fpp4"] = VARIANTS["fpp"] + VARIANTS["fpoly4"]
 VARIANTS["fpptrace"] = VARIANTS["fpp"] + VARIANTS["ftrace"]
 
