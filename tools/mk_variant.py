@@ -96,6 +96,17 @@ VARIANTS["bfmul2"] = [(B, "pk[(32 * h + c) >> 1] = pack2<F16>(pf.x * d.x, pf.y *
                        "const float2 ds = fmul2(pf, d);\n          pk[(32 * h + c) >> 1] = pack2<F16>(ds.x, ds.y);")]
 VARIANTS["bpoly0"] = [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)", "#define B_POLY(c) false")]
 VARIANTS["bfmul2p0"] = VARIANTS["bfmul2"] + VARIANTS["bpoly0"]
+# dQ staging: 3 x 8 KB (frees 8 KB of shared memory)
+VARIANTS["stage24k"] = [(B, "constexpr int DQ_BUFS = 4;\nconstexpr int DQ_ROWS = 64 / DQ_BUFS;",
+                         "constexpr int DQ_BUFS = 3;\nconstexpr int DQ_ROWS = 16;")]
+# fold descriptors with shared core matrices: ONES with SBO = 0 (every
+# 8-row group reads one 256 B block), EXT with LBO = 0 (K elements 8-15 read
+# the same 16 B as 0-7; ONES' zero half cancels them)
+VARIANTS["foldshare"] = [
+    (B, "const uint64_t ones_d = make_sdesc_noswz(sb + OFF_ONES, 128, 256);",
+        "const uint64_t ones_d = make_sdesc_noswz(sb + OFF_ONES, 128, 0);"),
+    (B, "make_sdesc_noswz(ext, sb + OFF_K - ext, 128)", "make_sdesc_noswz(ext, 0, 128)"),
+]
 VARIANTS["fpp4"] = VARIANTS["fpp"] + VARIANTS["fpoly4"]
 VARIANTS["fpptrace"] = VARIANTS["fpp"] + VARIANTS["ftrace"]
 
