@@ -33,8 +33,6 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
     # half the staging bytes in flight (2 x 8 KB instead of 4 x 8 KB)
     "stage16k": [(B, "constexpr int DQ_BUFS = 4;\nconstexpr int DQ_ROWS = 64 / DQ_BUFS;",
                   "constexpr int DQ_BUFS = 2;\nconstexpr int DQ_ROWS = 16;")],
-    # P phase: half of the exponential pairs on the FMA-pipe polynomial
-    "poly2": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)", "#define B_POLY(c) (((c) >> 1) & 1)")],
     # TMA tensor STORE instead of reduce-add (wrong results): the L2 RMW cost
     "dqstore": [(B, "          tma_reduce_add_3d_g(&tm_dq, buf, 0, qrow + DQ_ROWS * r, bh);",
                  "          asm volatile(\"cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group"
@@ -74,8 +72,6 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
     "bwdsleep": [(B, "#include \"kernels.h\"", "#include \"kernels.h\"\n#define mbar_wait mbar_wait_sleep")],
     # forward: the softmax warps' S-ready waits suspend-hinted too
     "fwdsleep": [(F, "#include \"kernels.h\"", "#include \"kernels.h\"\n#define mbar_wait mbar_wait_sleep")],
-    "poly38": [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)",
-                "#define B_POLY(c) ((((c) >> 1) & 7) == 1 || (((c) >> 1) & 7) == 4 || (((c) >> 1) & 7) == 6)")],
     # forward: the two softmax warpgroups take turns in the exponential phase
     # (named barriers 2/3, 256 threads): no MUFU sharing between the tiles
     "fpp": [(F, "      float tsum = exps(m_run == -INFINITY ? 0.f : m_run);",
@@ -91,22 +87,9 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
 }
 
 
-# backward dS = P (dP - delta) with one packed f32x2 multiply per pair
-VARIANTS["bfmul2"] = [(B, "pk[(32 * h + c) >> 1] = pack2<F16>(pf.x * d.x, pf.y * d.y);",
-                       "const float2 ds = fmul2(pf, d);\n          pk[(32 * h + c) >> 1] = pack2<F16>(ds.x, ds.y);")]
-VARIANTS["bpoly0"] = [(B, "#define B_POLY(c) ((((c) >> 1) & 3) == 3)", "#define B_POLY(c) false")]
-VARIANTS["bfmul2p0"] = VARIANTS["bfmul2"] + VARIANTS["bpoly0"]
 # dQ staging: 3 x 8 KB (frees 8 KB of shared memory)
 VARIANTS["stage24k"] = [(B, "constexpr int DQ_BUFS = 4;\nconstexpr int DQ_ROWS = 64 / DQ_BUFS;",
                          "constexpr int DQ_BUFS = 3;\nconstexpr int DQ_ROWS = 16;")]
-# fold descriptors with shared core matrices: ONES with SBO = 0 (every
-# 8-row group reads one 256 B block), EXT with LBO = 0 (K elements 8-15 read
-# the same 16 B as 0-7; ONES' zero half cancels them)
-VARIANTS["foldshare"] = [
-    (B, "const uint64_t ones_d = make_sdesc_noswz(sb + OFF_ONES, 128, 256);",
-        "const uint64_t ones_d = make_sdesc_noswz(sb + OFF_ONES, 128, 0);"),
-    (B, "make_sdesc_noswz(ext, sb + OFF_K - ext, 128)", "make_sdesc_noswz(ext, 0, 128)"),
-]
 VARIANTS["fpp4"] = VARIANTS["fpp"] + VARIANTS["fpoly4"]
 VARIANTS["fpptrace"] = VARIANTS["fpp"] + VARIANTS["ftrace"]
 
