@@ -54,19 +54,21 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapFloatOOBfill);
 
 template <int MODE, int DEPTH>
-void run(const CUtensorMap& tm, float* acc, int rows, long long* dcyc, const char* name) {
+void run(const CUtensorMap& tm, float* acc, int rows, long long* dcyc, const char* name,
+         int ctas = 148) {
   const int iters = 2048;
   auto kern = k<MODE, DEPTH>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * BOX_BYTES);
-  for (int rep = 0; rep < 2; ++rep) kern<<<148, 128, 4 * BOX_BYTES>>>(tm, acc, rows, iters, dcyc);
+  for (int rep = 0; rep < 2; ++rep) kern<<<ctas, 128, 4 * BOX_BYTES>>>(tm, acc, rows, iters, dcyc);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, dcyc, sizeof(h), cudaMemcpyDeviceToHost);
   double mean = 0;
-  for (int i = 0; i < 148; ++i) mean += h[i];
-  mean /= 148;
-  printf("%-42s depth %d: %6.1f B/clk per SM (%s)\n", name, DEPTH,
-         (double)iters * BOX_BYTES / mean, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+  for (int i = 0; i < ctas; ++i) mean += h[i];
+  mean /= ctas;
+  printf("%-42s depth %d, %3d CTAs, %4d MB target: %6.1f B/clk per SM (%s)\n", name, DEPTH, ctas,
+         int((long long)rows * COLS * 4 >> 20), (double)iters * BOX_BYTES / mean,
+         e == cudaSuccess ? "ok" : cudaGetErrorString(e));
 }
 
 int main() {
@@ -92,5 +94,19 @@ int main() {
   run<0, 1>(tm, acc, rows, dcyc, "TMA tensor reduce-add (8 KB boxes)");
   run<1, 4>(tm, acc, rows, dcyc, "1-D bulk reduce-add (8 KB)");
   run<2, 4>(tm, acc, rows, dcyc, "TMA tensor store (8 KB boxes, no reduction)");
+  // L2-resident target (32 MB: one head's dQ accumulator at N = 64K), and one SM alone
+  CUtensorMap tms;
+  const int rows_s = 65536;
+  cuuint64_t dims_s[3] = {COLS, (cuuint64_t)rows_s, 1};
+  cuuint64_t strides_s[2] = {COLS * 4, (cuuint64_t)rows_s * COLS * 4};
+  r = ((EncodeFn)fn)(&tms, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, acc, dims_s, strides_s, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return 1; }
+  run<0, 4>(tms, acc, rows_s, dcyc, "TMA tensor reduce-add (8 KB boxes)");
+  run<0, 4>(tms, acc, rows_s, dcyc, "TMA tensor reduce-add (8 KB boxes)", 1);
+  run<0, 4>(tms, acc, rows_s, dcyc, "TMA tensor reduce-add (8 KB boxes)", 16);
+  run<2, 4>(tms, acc, rows_s, dcyc, "TMA tensor store (8 KB boxes, no reduction)");
+  run<2, 4>(tms, acc, rows_s, dcyc, "TMA tensor store (8 KB boxes, no reduction)", 1);
   return 0;
 }
