@@ -15,7 +15,7 @@ using namespace a2d;
 
 constexpr int ROWS_PER_BOX = 16, COLS = 128, BOX_BYTES = ROWS_PER_BOX * COLS * 4;
 
-template <int MODE, int DEPTH>
+template <int MODE, int DEPTH, int REQ = BOX_BYTES>
 __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap tm, float* acc,
                                             int rows, int iters, long long* cyc) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -24,8 +24,40 @@ __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap 
   for (int i = threadIdx.x; i < 4 * BOX_BYTES / 4; i += blockDim.x) s[i] = 1e-3f;
   fence_proxy_async_smem();
   __syncthreads();
+  __shared__ __align__(8) uint64_t lbar[4];
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&lbar[i]), 1);
+  fence_mbar_init();
+  __syncthreads();
   if (threadIdx.x != 0) return;
   const int nbox = rows / ROWS_PER_BOX;
+  if (MODE >= 5) {  // 5: TMA tensor loads only; 6: loads and reduce-adds alternating
+    long long t0 = clock64();
+    int use[4] = {0, 0, 0, 0};
+    for (int it = 0; it < iters; ++it) {
+      const int box = (blockIdx.x * 37 + it) % nbox;
+      const int b = it & 3;
+      const uint32_t buf = sb + b * BOX_BYTES;
+      const bool load = MODE == 5 || (it & 1);
+      if (load) {
+        if (use[b] > 0) mbar_wait(smem_u32(&lbar[b]), (use[b] - 1) & 1);
+        bulk_wait_group_read<0>();
+        mbar_expect_tx(smem_u32(&lbar[b]), BOX_BYTES);
+        tma_load_3d(buf, &tm, smem_u32(&lbar[b]), 0, box * ROWS_PER_BOX, 0);
+        ++use[b];
+      } else {
+        if (use[b] > 0) mbar_wait(smem_u32(&lbar[b]), (use[b] - 1) & 1);
+        bulk_wait_group_read<1>();
+        tma_reduce_add_3d_g(&tm, buf, 0, box * ROWS_PER_BOX, 0);
+        bulk_commit_group();
+      }
+    }
+    for (int b = 0; b < 4; ++b)
+      if (use[b] > 0) mbar_wait(smem_u32(&lbar[b]), (use[b] - 1) & 1);
+    bulk_wait_group_all();
+    cyc[blockIdx.x] = clock64() - t0;
+    return;
+  }
   long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
     const int box = (blockIdx.x * 37 + it) % nbox;
@@ -35,8 +67,13 @@ __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap 
       tma_reduce_add_3d_g(&tm, buf, 0, box * ROWS_PER_BOX, 0);
     } else if (MODE == 1) {
       float* dst = acc + (long long)box * ROWS_PER_BOX * COLS;
+      // REQ-byte requests from a ring of 32 KB / REQ buffers
+      const int nb = 4 * BOX_BYTES / REQ;
+      const uint32_t b2 = sb + (it % nb) * REQ;
+      float* d2 = acc + ((long long)box * ROWS_PER_BOX * COLS) % ((long long)rows * COLS - REQ / 4);
       asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;"
-                   ::"l"(dst), "r"(buf), "r"(BOX_BYTES) : "memory");
+                   ::"l"(d2), "r"(b2), "r"(REQ) : "memory");
+      (void)dst;
     } else {
       asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group"
                    " [%0, {%2, %3, %4}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&tm)),
@@ -53,11 +90,11 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                              CUtensorMapFloatOOBfill);
 
-template <int MODE, int DEPTH>
+template <int MODE, int DEPTH, int REQ = BOX_BYTES>
 void run(const CUtensorMap& tm, float* acc, int rows, long long* dcyc, const char* name,
          int ctas = 148) {
   const int iters = 2048;
-  auto kern = k<MODE, DEPTH>;
+  auto kern = k<MODE, DEPTH, REQ>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * BOX_BYTES);
   for (int rep = 0; rep < 2; ++rep) kern<<<ctas, 128, 4 * BOX_BYTES>>>(tm, acc, rows, iters, dcyc);
   cudaError_t e = cudaDeviceSynchronize();
@@ -67,7 +104,7 @@ void run(const CUtensorMap& tm, float* acc, int rows, long long* dcyc, const cha
   for (int i = 0; i < ctas; ++i) mean += h[i];
   mean /= ctas;
   printf("%-42s depth %d, %3d CTAs, %4d MB target: %6.1f B/clk per SM (%s)\n", name, DEPTH, ctas,
-         int((long long)rows * COLS * 4 >> 20), (double)iters * BOX_BYTES / mean,
+         int((long long)rows * COLS * 4 >> 20), (double)iters * (MODE == 1 ? REQ : BOX_BYTES) / mean,
          e == cudaSuccess ? "ok" : cudaGetErrorString(e));
 }
 
@@ -108,5 +145,13 @@ int main() {
   run<0, 4>(tms, acc, rows_s, dcyc, "TMA tensor reduce-add (8 KB boxes)", 16);
   run<2, 4>(tms, acc, rows_s, dcyc, "TMA tensor store (8 KB boxes, no reduction)");
   run<2, 4>(tms, acc, rows_s, dcyc, "TMA tensor store (8 KB boxes, no reduction)", 1);
+  run<1, 4, 2048>(tms, acc, rows_s, dcyc, "1-D bulk reduce-add, 2 KB requests");
+  run<1, 4, 4096>(tms, acc, rows_s, dcyc, "1-D bulk reduce-add, 4 KB requests");
+  run<1, 2, 16384>(tms, acc, rows_s, dcyc, "1-D bulk reduce-add, 16 KB requests");
+  run<1, 1, 32768>(tms, acc, rows_s, dcyc, "1-D bulk reduce-add, 32 KB requests");
+  run<1, 8, 4096>(tms, acc, rows_s, dcyc, "1-D bulk reduce-add, 4 KB requests");
+  run<5, 4>(tms, acc, rows_s, dcyc, "TMA tensor load (8 KB boxes)");
+  run<5, 4>(tms, acc, rows_s, dcyc, "TMA tensor load (8 KB boxes)", 1);
+  run<6, 4>(tms, acc, rows_s, dcyc, "TMA loads + reduce-adds alternating (8 KB)");
   return 0;
 }

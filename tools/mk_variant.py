@@ -87,6 +87,19 @@ VARIANTS: dict[str, list[tuple[str, str, str]]] = {
 }
 
 
+# (bound, wrong results) Q / dO tiles loaded by TMA only for the first two
+# query tiles: what the per-SM TMA engine's load work costs the backward
+VARIANTS["noqload"] = [
+    (B, """            mbar_expect_tx(bar(B_QFULL0 + qs), TILE_B);
+            for (int s = 0; s < 2; ++s)""", """            mbar_expect_tx(bar(B_QFULL0 + qs), i < 2 ? TILE_B : 0);
+            for (int s = 0; s < 2 && i < 2; ++s)"""),
+    (B, """            mbar_expect_tx(bar(B_DOFULL), TILE_B);
+            for (int s = 0; s < 2; ++s)""", """            mbar_expect_tx(bar(B_DOFULL), i < 2 ? TILE_B : 0);
+            for (int s = 0; s < 2 && i < 2; ++s)"""),
+]
+# (bound, wrong results) only the dO loads skipped
+VARIANTS["nodoload"] = VARIANTS["noqload"][1:]
+
 # dQ staging: 3 x 8 KB (frees 8 KB of shared memory)
 VARIANTS["stage24k"] = [(B, "constexpr int DQ_BUFS = 4;\nconstexpr int DQ_ROWS = 64 / DQ_BUFS;",
                          "constexpr int DQ_BUFS = 3;\nconstexpr int DQ_ROWS = 16;")]
