@@ -33,6 +33,7 @@
 //   0 TMA producer, 1 MMA issuer, 2-3 idle                         (72 regs)
 //   4-7 P/dS warpgroup A (query columns 0-63), 8-11 B (64-127)     (136 regs)
 //   12-15 dQ drain: all 128 columns of Y in registers at once       (168 regs)
+#include <atomic>
 #include "sm100.cuh"
 #include "tiles.cuh"
 #include "kernels.h"
@@ -539,15 +540,17 @@ int bwd_q_tile_rows(int) { return TILE; }
 
 int launch_tile_bwd(const a2d_tile_bwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                   const CUtensorMap& tv, const CUtensorMap& tdo, cudaStream_t stream) {
-  static bool configured[2][64] = {};
+  // per (operand type, device): cudaFuncSetAttribute once (idempotent, so a
+  // racing first call from two host threads is harmless; atomic for the flag)
+  static std::atomic<bool> configured[2][64];
   const bool f16 = a.in_dtype == A2D_F16;
   auto kern = f16 ? bwd128_kernel<true> : bwd128_kernel<false>;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!configured[f16][dev & 63]) {
+  if (!configured[f16][dev & 63].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(bwd128)");
-    configured[f16][dev & 63] = true;
+    configured[f16][dev & 63].store(true, std::memory_order_release);
   }
   CUtensorMap tdq;
   int rc = make_map_f32_dq_flat(&tdq, a.dq_acc, a.h, a.nq, a.bh, a.dq_stride_row, a.dq_stride_bh,

@@ -26,6 +26,7 @@
 // Because tcgen05 MMAs of one thread complete in order and S_t(j)'s commit
 // is issued after PV_t(j-1), "S_t(j) full" also means "O_t holds PV_t(j-1)":
 // the rare rescale of O_t needs no extra barrier.
+#include <atomic>
 #include "sm100.cuh"
 #include "tiles.cuh"
 #include "kernels.h"
@@ -524,14 +525,14 @@ template <int HD, bool F16>
 int launch_fwd2_hd(const a2d_tile_fwd_args& a, const CUtensorMap& tq, const CUtensorMap& tk,
                    const CUtensorMap& tv, cudaStream_t stream) {
   using L = F2Layout<HD>;
-  static bool configured[64] = {false};
+  static std::atomic<bool> configured[64];  // see launch_tile_bwd
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!configured[dev & 63]) {
+  if (!configured[dev & 63].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(fwd2_kernel<HD, F16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fwd2)");
-    configured[dev & 63] = true;
+    configured[dev & 63].store(true, std::memory_order_release);
   }
   const int q_tiles = (a.q_map.mode == A2D_IDX_AFFINE && a.q_map.nblocks > 1)
                           ? a.q_map.nblocks * (a.q_map.rows_per_block / TILE)
